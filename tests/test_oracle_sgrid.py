@@ -1,0 +1,139 @@
+"""Pins of oracle/sgrid.py: combination technique, preconditioner, solver, and
+the paper's own printed numbers (no GPU)."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from sginputs import get_config
+from oracle.fem import gl01
+from oracle.exact import exact_fun, l2_error_2d
+from oracle.sgrid import SGProblem
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _injection(H, lc, lf):
+    """Nodal restriction (point evaluation of a fine P1 function at coarse nodes)."""
+    mc, mf = H.meshes[lc], H.meshes[lf]
+    idx = [mf.node_id[tuple((z * 2 ** (lf - lc)).tolist())] for z in mc.lattice]
+    return np.asarray(idx)
+
+
+def _interp_on(P, U, l):
+    """Nodal values on grid l of the sparse-grid function U (sum over its blocks)."""
+    out = np.zeros((P.Hx.n(l[0]), P.Hv.n(l[1])))
+    for lp, u in U.items():
+        if l[0] >= lp[0]:
+            A = P.Hx.E(l[0], lp[0]).toarray()
+        else:
+            A = np.eye(P.Hx.n(lp[0]))[_injection(P.Hx, l[0], lp[0])]
+        if l[1] >= lp[1]:
+            B = P.Hv.E(l[1], lp[1]).toarray()
+        else:
+            B = np.eye(P.Hv.n(lp[1]))[_injection(P.Hv, l[1], lp[1])]
+        out += A @ u[0] @ B.T
+    return out
+
+
+@pytest.mark.parametrize("name,L", [("c0_2d_const", 5), ("c3_4d_lshape", 4), ("c4_6d_stream", 3)])
+def test_combination_reproduces_sparse_grid_functions(name, L):
+    """(d) PAPER.md l.557-566: the combination of the nodal interpolants on |l|=L, L-1
+    reproduces any f in V_L exactly ('for interpolation ... gives the exact result')."""
+    P = SGProblem(get_config(name, L=L))
+    rng = np.random.default_rng(3)
+    f = {l: rng.standard_normal((1,) + P.shape(l)[1:]) for l in P.active}
+    dhat = {l: _interp_on(P, f, l)[None] for l in P.active + P.coarse}
+    g = P.combine(dhat)
+    full_f = P.to_full(f); full_g = P.to_full(g)
+    assert np.abs(full_f - full_g).max() <= 1e-12 * np.abs(full_f).max()
+
+
+def test_single_grid_preconditioner_is_exact():
+    """L=2: one component grid, P^{-1} = A^{-1}: Richardson converges in one step."""
+    P = SGProblem(get_config("c1_2d_rot", L=2))
+    rng = np.random.default_rng(4)
+    b = {l: rng.standard_normal(P.shape(l)) for l in P.active}
+    u, it, hist = P.solve_strip(b, rtol=1e-13)
+    assert it <= 2 and hist[-1] <= 1e-12 * max(hist[0], 1e-300) + 1e-300
+    r = P.apply_full(P.terms, u)
+    for l in P.active:
+        assert np.abs(r[l] - b[l]).max() <= 1e-12 * np.abs(b[l]).max()
+
+
+def test_pure_mass_strip_is_l2_projection():
+    """beta = 0, sigma = 0 (f=g=0): a(U,w) = G^t(x)M + ... reduces to the jump term; the
+    strip solution is constant in time and equal to the previous trace (SPEC strip_assembly)."""
+    cfg = get_config("c1_2d_rot", L=5, q=1)
+    cfg["beta"] = []
+    P = SGProblem(cfg)
+    tr0 = P.interp_u0()
+    b = P.rhs(1, tr0)
+    U, it, _ = P.solve_strip(b, rtol=1e-13)
+    tr1 = P.trace(U)
+    # compare FUNCTIONS (spanning set: coefficients are not unique) on the full grid
+    f0, f1 = P.to_full(tr0), P.to_full(tr1)
+    assert np.abs(f1 - f0).max() <= 1e-12 * np.abs(f0).max()
+    # time-constant: the eta_1 coefficients represent the zero function
+    U1 = {l: U[l][1:2] for l in P.active}
+    assert np.abs(P.to_full(U1)).max() <= 1e-12 * np.abs(f0).max()
+
+
+def test_solution_satisfies_galerkin_system():
+    """Converged Richardson iterate: ||A u - b|| small relative to ||b|| on every block
+    (b is in the range of A)."""
+    P = SGProblem(get_config("c0_2d_const", L=5, q=1))
+    tr0 = P.interp_u0()
+    b = P.rhs(1, tr0)
+    u, it, hist = P.solve_strip(b, rtol=1e-13)
+    r = P.apply_full(P.terms, u)
+    nb = max(np.abs(b[l]).max() for l in P.active)
+    assert max(np.abs(r[l] - b[l]).max() for l in P.active) <= 1e-10 * nb
+    assert it < 60
+
+
+def test_paper_table1_d1_r1():
+    """Golden: PAPER.md Table 1 (l.597-628), d=1, r=1, L=2..4 within 10% (SPEC asks factor 2)."""
+    gold = json.load(open(os.path.join(GOLD, "paper_table1_d1_r1.json")))
+    for Lp in (2, 3, 4):
+        cfg = dict(name="table1", d=1, xmesh=dict(kind="periodic", lo=[0.0], hi=[1.0]),
+                   vmesh=dict(kind="periodic", lo=[0.0], hi=[1.0]), nc=4, L=Lp + 1, q=1,
+                   tau=0.5 / 2 ** (Lp + 1), T=0.5, nsteps=2 ** (Lp + 1), sigma=0.0,
+                   beta=[(0, {(0,): 1.0}, {(0,): 1.0}), (1, {(0,): 1.0}, {(0,): 1.0})],
+                   u0=[(1.0, {"type": "sin", "k": 1}, {"type": "cos", "k": 1}),
+                       (1.0, {"type": "cos", "k": 1}, {"type": "sin", "k": 1})], g=None)
+        P = SGProblem(cfg)
+        tr, U, it = P.run()
+        Uf = P.to_full(tr)
+        n = P.Hx.n(P.F); h = 1.0 / n; g, w = gl01(4)
+        e2 = n2 = 0.0
+        a = g[:, None]; bb = g[None, :]
+        for i in range(n):
+            for k in range(n):
+                Ui = ((1 - a) * (1 - bb) * Uf[i, k] + a * (1 - bb) * Uf[(i + 1) % n, k]
+                      + (1 - a) * bb * Uf[i, (k + 1) % n] + a * bb * Uf[(i + 1) % n, (k + 1) % n])
+                E = np.sin(2 * np.pi * ((i + a) * h + (k + bb) * h))
+                W = np.outer(w, w) * h * h
+                e2 += np.sum(W * (Ui - E) ** 2); n2 += np.sum(W * E ** 2)
+        rel = math.sqrt(e2 / n2)
+        ref = gold["rel_err"][Lp - 1]
+        assert 0.8 * ref <= rel <= 1.2 * ref, (Lp, rel, ref)
+
+
+def test_convergence_rate_vs_characteristics():
+    """(e) error vs the exact characteristic solution u0(r - beta t) (configs[0] family,
+    wide Gaussian, dG(1), tau ~ h): observed order >= s + 1/2 = 1.5 (Thm 4, l.325-329)."""
+    errs = []
+    for L in (4, 5, 6):
+        cfg = get_config("c0_2d_const", L=L, q=1)
+        for t in cfg["u0"]:
+            t[1]["w"] = 0.1; t[2]["w"] = 0.1
+        cfg["tau"] = 2.0 ** -(L - 1); cfg["T"] = 0.25; cfg["nsteps"] = int(round(0.25 / cfg["tau"]))
+        P = SGProblem(cfg)
+        tr, U, it = P.run()
+        e, n = l2_error_2d(P, P.to_full(tr), exact_fun(cfg, cfg["nsteps"] * cfg["tau"]))
+        errs.append(e / n)
+    rates = [math.log2(errs[i] / errs[i + 1]) for i in range(len(errs) - 1)]
+    assert errs[-1] < 1.5e-2 and min(rates) >= 1.5, (errs, rates)
