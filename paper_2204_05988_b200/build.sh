@@ -1,0 +1,16 @@
+#!/bin/bash
+# Build libsg.so for sm_100a (B200).  Usage: build.sh [extra nvcc flags]
+set -e
+HERE="$(cd "$(dirname "$0")" && pwd)"
+cd "$HERE/csrc"
+NVCC=${NVCC:-/usr/local/cuda/bin/nvcc}
+FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr $*"
+OBJS=""
+for f in mesh assemble kernels setup solver api; do
+  $NVCC $FLAGS -dc -o "$f.o" "$f.cu" &
+  OBJS="$OBJS $f.o"
+done
+wait
+$NVCC -gencode arch=compute_100a,code=sm_100a -shared -o "$HERE/libsg.so" $OBJS -lcudart
+rm -f $OBJS
+echo "built $HERE/libsg.so"

@@ -1,0 +1,466 @@
+// C ABI of libsg (include/sg.h).  Argument checking, allocation, dispatch.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+#include "sg_internal.cuh"
+
+namespace sg {
+const char* last_error();
+int expand_terms(sg_problem* P);
+int combine_group(sg_problem* P, Group& g, bool other_is_x);
+int combine(sg_problem* P, int S, const double* dhat_a, const double* dhat_c, double* du);
+int interp_u0(sg_problem* P, double* u);
+int rhs(sg_problem* P, int j, const double* trace, double* b);
+int solve_strip(sg_problem* P, const double* b, double* u, double rtol, double inner_rtol, int max_iter, int* iters,
+                double* last);
+int step(sg_problem* P, int j0, int nsteps, double* trace_dev, double rtol, double inner_rtol);
+}  // namespace sg
+
+using namespace sg;
+
+#define CHECK_ARG(cond, msg)      \
+    do {                          \
+        if (!(cond)) {            \
+            set_error(msg);       \
+            return SG_ERR_ARG;    \
+        }                         \
+    } while (0)
+
+extern "C" const char* sg_last_error(void) { return last_error(); }
+
+extern "C" int sg_create(const sg_config* cfg, void* stream, sg_problem** out) {
+    CHECK_ARG(cfg && out, "null argument");
+    *out = nullptr;
+    CHECK_ARG(cfg->d >= 1 && cfg->d <= 3, "d must be 1..3");
+    CHECK_ARG(cfg->L >= 2 && cfg->L <= 40, "L must be >= 2");
+    CHECK_ARG(cfg->q == 0 || cfg->q == 1, "q must be 0 or 1");
+    CHECK_ARG(cfg->nc >= 1, "nc >= 1");
+    CHECK_ARG(cfg->tau > 0, "tau > 0");
+    CHECK_ARG(cfg->nbeta >= 0 && cfg->nbeta <= 6 && cfg->nu0 >= 0 && cfg->nu0 <= 4, "nbeta <= 6, nu0 <= 4");
+    CHECK_ARG(cfg->xkind == SG_MESH_BOX || (cfg->xkind == SG_MESH_LSHAPE && cfg->d == 2), "xkind");
+    CHECK_ARG(cfg->vkind == SG_MESH_BOX || (cfg->vkind == SG_MESH_LSHAPE && cfg->d == 2), "vkind");
+    CHECK_ARG(cfg->inflow == 0 || cfg->d == 1, "inflow data only for d = 1");
+    for (int i = 0; i < cfg->nbeta; ++i) CHECK_ARG(cfg->beta[i].axis >= 0 && cfg->beta[i].axis < 2 * cfg->d, "beta axis");
+    for (int i = 0; i < cfg->d; ++i) CHECK_ARG(cfg->xhi[i] > cfg->xlo[i] && cfg->vhi[i] > cfg->vlo[i], "domain bounds");
+    if ((cfg->xkind == SG_MESH_LSHAPE || cfg->vkind == SG_MESH_LSHAPE) && (cfg->nc % 2) != 0) {
+        set_error("L-shape needs an even number of level-1 cells");
+        return SG_ERR_ARG;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        set_error("no CUDA device: libsg has no CPU fallback");
+        return SG_ERR_CUDA;
+    }
+    sg_problem* P = new (std::nothrow) sg_problem();
+    if (!P) return SG_ERR_STATE;
+    P->cfg = *cfg;
+    P->stream = (cudaStream_t)stream;
+    P->verbose = getenv("SG_VERBOSE") != nullptr;
+    P->S = cfg->q + 1;
+    P->F = cfg->L - 1;
+    auto setf = [&](Factor& f, int kind, const double* lo, const double* hi) {
+        f.kind = kind;
+        f.d = cfg->d;
+        f.nc = cfg->nc;
+        for (int i = 0; i < 3; ++i) {
+            f.lo[i] = i < cfg->d ? lo[i] : 0.0;
+            f.hi[i] = i < cfg->d ? hi[i] : 0.0;
+        }
+        f.W = (1 << (cfg->d + 1)) - 1;
+    };
+    setf(P->fx, cfg->xkind, cfg->xlo, cfg->xhi);
+    setf(P->fv, cfg->vkind, cfg->vlo, cfg->vhi);
+    // delta = finest edge length (reading R5)
+    if (cfg->delta > 0) {
+        P->delta = cfg->delta;
+    } else {
+        const double cells = (double)(cfg->nc) * std::ldexp(1.0, P->F - 1);
+        double h = 1e300;
+        for (int i = 0; i < cfg->d; ++i) {
+            h = std::min(h, (cfg->xhi[i] - cfg->xlo[i]) / cells);
+            h = std::min(h, (cfg->vhi[i] - cfg->vlo[i]) / cells);
+        }
+        P->delta = h;
+    }
+    int rc = expand_terms(P);
+    if (rc != SG_OK) {
+        delete P;
+        return rc;
+    }
+    *out = P;
+    return SG_OK;
+}
+
+extern "C" int sg_build_meshes(sg_problem* P) {
+    CHECK_ARG(P, "null handle");
+    if (P->meshes_built) return SG_OK;
+    SG_TRY(build_factor_meshes(P, P->fx, P->F));
+    SG_TRY(build_factor_meshes(P, P->fv, P->F));
+    SG_CUDA(cudaStreamSynchronize(P->stream));
+    // component grids
+    const int L = P->cfg.L;
+    int64_t off = 0;
+    P->active.clear();
+    P->coarse.clear();
+    for (int l1 = 1; l1 <= L - 1; ++l1) {
+        Grid g{l1, L - l1, P->fx.lev[l1].n, P->fv.lev[L - l1].n, off};
+        off += g.n1 * g.n2;
+        P->active.push_back(g);
+    }
+    off = 0;
+    for (int l1 = 1; l1 <= L - 2; ++l1) {
+        Grid g{l1, L - 1 - l1, P->fx.lev[l1].n, P->fv.lev[L - 1 - l1].n, off};
+        off += g.n1 * g.n2;
+        P->coarse.push_back(g);
+    }
+    if (P->active.size() + P->coarse.size() > (size_t)MAX_SEG) {
+        set_error("too many component grids");
+        return SG_ERR_UNSUPPORTED;
+    }
+    P->meshes_built = true;
+    return SG_OK;
+}
+
+extern "C" int sg_assemble_factors(sg_problem* P) {
+    CHECK_ARG(P, "null handle");
+    if (!P->meshes_built) {
+        set_error("sg_build_meshes first");
+        return SG_ERR_STATE;
+    }
+    if (P->assembled) return SG_OK;
+    const int F = P->F, S = P->S, L = P->cfg.L;
+    for (int l = 1; l <= F; ++l) {
+        SG_TRY(assemble_spec(P, P->fx, P->mass_x, l));
+        SG_TRY(assemble_spec(P, P->fv, P->mass_v, l));
+        for (auto& g : P->vgroups) SG_TRY(assemble_spec(P, P->fv, g.spec, l));
+        for (auto& g : P->xgroups) SG_TRY(assemble_spec(P, P->fx, g.spec, l));
+    }
+    for (auto& g : P->vgroups) SG_TRY(combine_group(P, g, true));
+    for (auto& g : P->xgroups) SG_TRY(combine_group(P, g, false));
+    // workspaces
+    int64_t maxg = 0;
+    for (auto& g : P->active) maxg = std::max(maxg, g.n1 * g.n2);
+    for (auto& g : P->coarse) maxg = std::max(maxg, g.n1 * g.n2);
+    const int ng = (int)P->active.size();
+    int64_t chain = 0, chain_up = 0;
+    for (int pp = 1; pp <= ng; ++pp)
+        for (int k = 0; k <= ng - pp; ++k) chain += P->fx.lev[pp].n * P->fv.lev[L - pp - k].n;
+    for (int pp = 2; pp <= ng; ++pp)
+        for (int k = 0; k <= pp - 1; ++k) chain_up += P->fx.lev[pp - k].n * P->fv.lev[L - pp].n;
+    const size_t nbz = std::max(P->vgroups.size(), (size_t)1);
+    P->wsZ_n = (size_t)std::max<int64_t>(std::max<int64_t>(nbz * S * maxg, S * chain), S * chain_up);
+    P->wsA_n = P->wsB_n = (size_t)(S * maxg);
+    SG_CUDA(cudaMalloc(&P->wsZ, sizeof(double) * P->wsZ_n));
+    SG_CUDA(cudaMalloc(&P->wsA, sizeof(double) * P->wsA_n));
+    SG_CUDA(cudaMalloc(&P->wsB, sizeof(double) * P->wsB_n));
+    const int64_t Na = set_size(P, SG_SET_ACTIVE, S), Nc = set_size(P, SG_SET_COARSE, S);
+    const int64_t nblk = (Na + Nc) / 2048 + 2 * MAX_SEG + 8;
+    SG_CUDA(cudaMalloc(&P->red, sizeof(double) * 3 * nblk));
+    SG_CUDA(cudaMalloc(&P->scal, sizeof(double) * 10 * (MAX_SEG + 1)));
+    SG_CUDA(cudaMemset(P->scal, 0, sizeof(double) * 10 * (MAX_SEG + 1)));
+    SG_CUDA(cudaMallocHost(&P->hscal, sizeof(double) * 10 * (MAX_SEG + 1)));
+    const int64_t nF = std::max(P->fx.lev[F].n, P->fv.lev[F].n) + 16;
+    const int64_t sizes[13] = {Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na, Na + Nc, Na + Nc, Na,
+                               std::max(Na, 4 * nF), Na, Na};
+    P->vec.assign(13, nullptr);
+    for (int i = 0; i < 13; ++i) SG_CUDA(cudaMalloc(&P->vec[i], sizeof(double) * sizes[i]));
+    SG_CUDA(cudaMalloc(&P->trace_dev, sizeof(double) * set_size(P, SG_SET_ACTIVE, 1)));
+    SG_CUDA(cudaStreamSynchronize(P->stream));
+    P->assembled = true;
+    return SG_OK;
+}
+
+static void free_level(Level& L) {
+    cudaFree(L.lat); cudaFree(L.cols); cudaFree(L.pcols); cudaFree(L.pvals); cudaFree(L.rcols); cudaFree(L.rvals);
+    for (double* p : L.fm) cudaFree(p);
+}
+
+extern "C" void sg_destroy(sg_problem* P) {
+    if (!P) return;
+    cudaStreamSynchronize(P->stream);
+    for (auto& L : P->fx.lev) free_level(L);
+    for (auto& L : P->fv.lev) free_level(L);
+    for (auto* gs : {&P->vgroups, &P->xgroups})
+        for (auto& g : *gs)
+            for (auto& lv : g.comb)
+                for (auto& ce : lv) cudaFree(ce.vals);
+    cudaFree(P->wsZ); cudaFree(P->wsA); cudaFree(P->wsB); cudaFree(P->red); cudaFree(P->scal);
+    if (P->hscal) cudaFreeHost(P->hscal);
+    for (double* v : P->vec) cudaFree(v);
+    cudaFree(P->trace_dev);
+    for (auto& pr : P->ev_pairs) {
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+    }
+    delete P;
+}
+
+// ---------------------------------------------------------------- queries
+extern "C" int sg_S(const sg_problem* P) { return P ? P->S : -1; }
+extern "C" double sg_delta(const sg_problem* P) { return P ? P->delta : -1.0; }
+extern "C" int sg_num_grids(const sg_problem* P, int set) {
+    if (!P) return -1;
+    if (set == SG_SET_ACTIVE) return P->cfg.L - 1;
+    return P->cfg.L - 2;
+}
+extern "C" int sg_grid_info(const sg_problem* P, int set, int g, int* l1, int* l2, int64_t* n1, int64_t* n2) {
+    CHECK_ARG(P && P->meshes_built, "handle / meshes");
+    const auto& gs = set == SG_SET_ACTIVE ? P->active : P->coarse;
+    CHECK_ARG(g >= 0 && g < (int)gs.size(), "grid index");
+    if (l1) *l1 = gs[g].l1;
+    if (l2) *l2 = gs[g].l2;
+    if (n1) *n1 = gs[g].n1;
+    if (n2) *n2 = gs[g].n2;
+    return SG_OK;
+}
+extern "C" int64_t sg_grid_offset(const sg_problem* P, int set, int g, int S_vec) {
+    if (!P || !P->meshes_built) return -1;
+    const auto& gs = set == SG_SET_ACTIVE ? P->active : P->coarse;
+    if (g < 0 || g >= (int)gs.size()) return -1;
+    return gs[g].off1 * S_vec;
+}
+extern "C" int64_t sg_set_size(const sg_problem* P, int set, int S_vec) {
+    if (!P || !P->meshes_built) return -1;
+    return set_size(P, set, S_vec);
+}
+static const Factor* factor_of(const sg_problem* P, int f) { return f == SG_FACTOR_X ? &P->fx : &P->fv; }
+
+extern "C" int sg_mesh_info(const sg_problem* P, int factor, int level, int64_t* n, int* width, int* m) {
+    CHECK_ARG(P && P->meshes_built, "handle / meshes");
+    const Factor* f = factor_of(P, factor);
+    CHECK_ARG(level >= 1 && level <= P->F, "level");
+    if (n) *n = f->lev[level].n;
+    if (width) *width = f->W;
+    if (m) *m = f->lev[level].m;
+    return SG_OK;
+}
+
+template <typename T>
+static int ell_to_host_rowmajor(const T* dev, int64_t n, int W, T* host) {
+    std::vector<T> tmp((size_t)n * W);
+    SG_CUDA(cudaMemcpy(tmp.data(), dev, sizeof(T) * n * W, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < n; ++i)
+        for (int k = 0; k < W; ++k) host[i * W + k] = tmp[(size_t)k * n + i];
+    return SG_OK;
+}
+
+extern "C" int sg_mesh_export(const sg_problem* P, int factor, int level, int32_t* lattice, int32_t* cols) {
+    CHECK_ARG(P && P->meshes_built, "handle / meshes");
+    CHECK_ARG(level >= 1 && level <= P->F, "level");
+    const Factor* f = factor_of(P, factor);
+    const Level& L = f->lev[level];
+    SG_CUDA(cudaStreamSynchronize(P->stream));
+    if (lattice) SG_TRY(ell_to_host_rowmajor<int32_t>(L.lat, L.n, f->d, lattice));
+    if (cols) SG_TRY(ell_to_host_rowmajor<int32_t>(L.cols, L.n, f->W, cols));
+    return SG_OK;
+}
+
+extern "C" int sg_transfer_export(const sg_problem* P, int factor, int level, int32_t* pcols, double* pvals,
+                                  int32_t* rcols, double* rvals) {
+    CHECK_ARG(P && P->meshes_built, "handle / meshes");
+    CHECK_ARG(level >= 2 && level <= P->F, "level");
+    const Factor* f = factor_of(P, factor);
+    const Level& L = f->lev[level];
+    const Level& C = f->lev[level - 1];
+    SG_CUDA(cudaStreamSynchronize(P->stream));
+    if (pcols) SG_TRY(ell_to_host_rowmajor<int32_t>(L.pcols, L.n, 2, pcols));
+    if (pvals) SG_TRY(ell_to_host_rowmajor<double>(L.pvals, L.n, 2, pvals));
+    if (rcols) SG_TRY(ell_to_host_rowmajor<int32_t>(L.rcols, C.n, f->W, rcols));
+    if (rvals) SG_TRY(ell_to_host_rowmajor<double>(L.rvals, C.n, f->W, rvals));
+    return SG_OK;
+}
+
+extern "C" int sg_num_terms(const sg_problem* P) { return P ? (int)P->terms.size() : -1; }
+extern "C" int sg_term_info(const sg_problem* P, int t, double* Tblock, int* xspec, int* vspec) {
+    CHECK_ARG(P && t >= 0 && t < (int)P->terms.size(), "term index");
+    if (Tblock)
+        for (int i = 0; i < P->S * P->S; ++i) Tblock[i] = P->terms[t].T[i];
+    if (xspec) *xspec = P->terms[t].xs;
+    if (vspec) *vspec = P->terms[t].vs;
+    return SG_OK;
+}
+extern "C" int sg_num_specs(const sg_problem* P, int factor) {
+    return P ? (int)factor_of(P, factor)->specs.size() : -1;
+}
+extern "C" int sg_spec_info(const sg_problem* P, int factor, int spec, int* kind, double* weight, int* trial_d,
+                            int* test_d, int* chi_axis, int* chi_sign, int* face_axis, int* face_sign) {
+    CHECK_ARG(P, "null handle");
+    const Factor* f = factor_of(P, factor);
+    CHECK_ARG(spec >= 0 && spec < (int)f->specs.size(), "spec index");
+    const Spec& s = f->specs[spec];
+    if (kind) *kind = s.kind;
+    if (weight)
+        for (int i = 0; i < NPOLY; ++i) weight[i] = s.w[i];
+    if (trial_d) *trial_d = s.trial_d;
+    if (test_d) *test_d = s.test_d;
+    if (chi_axis) *chi_axis = s.chi_axis;
+    if (chi_sign) *chi_sign = s.chi_sign;
+    if (face_axis) *face_axis = s.face_axis;
+    if (face_sign) *face_sign = s.face_sign;
+    return SG_OK;
+}
+extern "C" int sg_factor_export(const sg_problem* P, int factor, int spec, int level, double* vals) {
+    CHECK_ARG(P && P->assembled, "handle / assembly");
+    const Factor* f = factor_of(P, factor);
+    CHECK_ARG(level >= 1 && level <= P->F && spec >= 0 && spec < (int)f->specs.size(), "spec / level");
+    const Level& L = f->lev[level];
+    if (spec >= (int)L.fm.size() || !L.fm[spec]) {
+        set_error("factor matrix not assembled (unused spec)");
+        return SG_ERR_STATE;
+    }
+    SG_CUDA(cudaStreamSynchronize(P->stream));
+    return ell_to_host_rowmajor<double>(L.fm[spec], L.n, f->W, vals);
+}
+
+// ---------------------------------------------------------------- hot path
+#define NEED_ASSEMBLED(P)                                       \
+    do {                                                        \
+        CHECK_ARG(P, "null handle");                            \
+        if (!(P)->assembled) {                                  \
+            set_error("sg_assemble_factors first");             \
+            return SG_ERR_STATE;                                \
+        }                                                       \
+    } while (0)
+
+extern "C" int sg_apply_strip_operator(sg_problem* P, int set, int g, const double* X, double* Y) {
+    NEED_ASSEMBLED(P);
+    const auto& gs = set == SG_SET_ACTIVE ? P->active : P->coarse;
+    CHECK_ARG(g >= 0 && g < (int)gs.size(), "grid index");
+    CHECK_ARG(X && Y && X != Y, "X, Y must be distinct device pointers");
+    return apply_diag(P, gs[g], X, Y);
+}
+
+extern "C" int sg_apply_full(sg_problem* P, const double* X, double* Y) {
+    NEED_ASSEMBLED(P);
+    CHECK_ARG(X && Y && X != Y, "X, Y");
+    return apply_cross(P, nullptr, nullptr, P->S, P->S, X, Y);
+}
+
+extern "C" int sg_apply_mass_full(sg_problem* P, const double* Tb, int S_out, int S_in, const double* X, double* Y) {
+    NEED_ASSEMBLED(P);
+    CHECK_ARG(Tb && X && Y && X != Y, "args");
+    CHECK_ARG(S_out >= 1 && S_out <= MAXS && S_in >= 1 && S_in <= MAXS, "S_out/S_in");
+    return apply_cross(P, nullptr, Tb, S_out, S_in, X, Y);
+}
+
+static int transfer(sg_problem* P, int factor, int lf, int lc, int level_other, int S, const double* in, double* out,
+                    double beta, bool prolong) {
+    NEED_ASSEMBLED(P);
+    CHECK_ARG(lf == lc + 1, "transfers are one level at a time (lf = lc + 1)");
+    CHECK_ARG(lc >= 1 && lf <= P->F && level_other >= 1 && level_other <= P->F, "levels");
+    CHECK_ARG(S >= 1 && S <= MAXS && in && out && in != out, "args");
+    Factor& f = factor == SG_FACTOR_X ? P->fx : P->fv;
+    Factor& o = factor == SG_FACTOR_X ? P->fv : P->fx;
+    const int64_t no = o.lev[level_other].n;
+    const int dir = factor == SG_FACTOR_X ? 0 : 1;
+    const Level& F_ = f.lev[lf];
+    const int64_t nin = prolong ? f.lev[lc].n : F_.n, nout = prolong ? F_.n : f.lev[lc].n;
+    EntryList el;
+    el.ne = 0;
+    for (int s = 0; s < S; ++s) el.e[el.ne++] = {in, prolong ? F_.pvals : F_.rvals, 1.0, s, s};
+    const int W = prolong ? 2 : f.W;
+    const int32_t* cols = prolong ? F_.pcols : F_.rcols;
+    if (dir == 0) return launch_gather(P, 0, W, S, nin, no, nout, cols, el, out, beta);
+    return launch_gather(P, 1, W, S, no, nin, nout, cols, el, out, beta);
+}
+
+extern "C" int sg_prolongate(sg_problem* P, int factor, int lf, int lc, int level_other, int S, const double* in,
+                             double* out, double beta) {
+    return transfer(P, factor, lf, lc, level_other, S, in, out, beta, true);
+}
+extern "C" int sg_restrict(sg_problem* P, int factor, int lc, int lf, int level_other, int S, const double* in,
+                           double* out, double beta) {
+    return transfer(P, factor, lf, lc, level_other, S, in, out, beta, false);
+}
+
+extern "C" int sg_combine(sg_problem* P, const double* dhat_active, const double* dhat_coarse, double* du) {
+    NEED_ASSEMBLED(P);
+    CHECK_ARG(dhat_active && du && (dhat_coarse || P->coarse.empty()), "args");
+    return combine(P, P->S, dhat_active, dhat_coarse, du);
+}
+
+extern "C" int sg_interp_u0(sg_problem* P, double* u) {
+    NEED_ASSEMBLED(P);
+    CHECK_ARG(u, "u");
+    return interp_u0(P, u);
+}
+
+extern "C" int sg_rhs(sg_problem* P, int j, const double* trace_prev, double* b) {
+    NEED_ASSEMBLED(P);
+    CHECK_ARG(j >= 1 && trace_prev && b, "args");
+    return rhs(P, j, trace_prev, b);
+}
+
+extern "C" int sg_solve_strip(sg_problem* P, const double* b, double* u, double rtol, double inner_rtol, int max_iter,
+                              int* iters, double* last_norm) {
+    NEED_ASSEMBLED(P);
+    CHECK_ARG(b && u && b != u && rtol > 0 && inner_rtol > 0 && max_iter > 0, "args");
+    return solve_strip(P, b, u, rtol, inner_rtol, max_iter, iters, last_norm);
+}
+
+extern "C" int sg_step(sg_problem* P, int j0, int nsteps, double* trace, double rtol, double inner_rtol) {
+    NEED_ASSEMBLED(P);
+    CHECK_ARG(trace && j0 >= 1 && nsteps >= 0 && rtol > 0 && inner_rtol > 0, "args");
+    cudaPointerAttributes at;
+    bool host = true;
+    if (cudaPointerGetAttributes(&at, trace) == cudaSuccess && at.type == cudaMemoryTypeDevice) host = false;
+    cudaGetLastError();
+    const int64_t n = set_size(P, SG_SET_ACTIVE, 1);
+    double* tr = host ? P->trace_dev : trace;
+    if (host) SG_CUDA(cudaMemcpyAsync(tr, trace, sizeof(double) * n, cudaMemcpyHostToDevice, P->stream));
+    SG_TRY(step(P, j0, nsteps, tr, rtol, inner_rtol));
+    if (host) SG_CUDA(cudaMemcpyAsync(trace, tr, sizeof(double) * n, cudaMemcpyDeviceToHost, P->stream));
+    SG_CUDA(cudaStreamSynchronize(P->stream));
+    return SG_OK;
+}
+
+// ---------------------------------------------------------- instrumentation
+extern "C" int sg_stats(const sg_problem* P, int64_t* n_applies, int64_t* dof_applied, int64_t* launches,
+                        int64_t* outer_iters, int64_t* inner_iters) {
+    CHECK_ARG(P, "null handle");
+    if (n_applies) *n_applies = P->n_applies;
+    if (dof_applied) *dof_applied = P->dof_applied;
+    if (launches) *launches = P->launches;
+    if (outer_iters) *outer_iters = P->outer_iters;
+    if (inner_iters) *inner_iters = P->inner_iters;
+    return SG_OK;
+}
+extern "C" int sg_reset_stats(sg_problem* P) {
+    CHECK_ARG(P, "null handle");
+    P->n_applies = P->dof_applied = P->launches = P->outer_iters = P->inner_iters = 0;
+    SG_CUDA(cudaStreamSynchronize(P->stream));
+    for (auto& pr : P->ev_pairs) {
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+    }
+    P->ev_pairs.clear();
+    P->kern_ms = 0;
+    P->kern_launches = 0;
+    P->kern_bytes = P->kern_flops = 0;
+    return SG_OK;
+}
+extern "C" int sg_set_timing(sg_problem* P, int on) {
+    CHECK_ARG(P, "null handle");
+    P->timing = on != 0;
+    return SG_OK;
+}
+extern "C" int sg_kernel_time(sg_problem* P, double* ms, int64_t* launches, double* alg_bytes, double* alg_flops) {
+    CHECK_ARG(P, "null handle");
+    SG_CUDA(cudaStreamSynchronize(P->stream));
+    for (auto& pr : P->ev_pairs) {
+        float t = 0;
+        SG_CUDA(cudaEventElapsedTime(&t, pr.first, pr.second));
+        P->kern_ms += t;
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+    }
+    P->ev_pairs.clear();
+    if (ms) *ms = P->kern_ms;
+    if (launches) *launches = P->kern_launches;
+    if (alg_bytes) *alg_bytes = P->kern_bytes;
+    if (alg_flops) *alg_flops = P->kern_flops;
+    return SG_OK;
+}

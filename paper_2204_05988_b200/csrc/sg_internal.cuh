@@ -1,0 +1,166 @@
+// Internal data structures of libsg (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sg.h"
+
+namespace sg {
+
+constexpr int MAXD = 3;
+constexpr int NPOLY = 10;   // [1, y0, y1, y2, y0y0, y0y1, y0y2, y1y1, y1y2, y2y2]
+constexpr int MAXS = 2;     // q <= 1
+constexpr int MAX_ENTRIES = 64;
+constexpr int MAX_FANOUT = 12;
+constexpr int MAX_SEG = 64;
+
+void set_error(const std::string& msg);
+#define SG_CUDA(call)                                                                  \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess) {                                                       \
+            ::sg::set_error(std::string(#call) + ": " + cudaGetErrorString(e_));      \
+            return SG_ERR_CUDA;                                                        \
+        }                                                                              \
+    } while (0)
+#define SG_TRY(call)                 \
+    do {                             \
+        int r_ = (call);             \
+        if (r_ != SG_OK) return r_;  \
+    } while (0)
+
+// Factor matrix spec (eq. (14); see oracle/fem.py for the same definition)
+struct Spec {
+    int kind = 0;          // 0 vol, 1 face
+    double w[NPOLY] = {0}; // polynomial weight
+    int trial_d = -1, test_d = -1;
+    int chi_axis = -1, chi_sign = 0;
+    int face_axis = -1, face_sign = 0;
+    bool same(const Spec& o) const;
+};
+
+struct Term {
+    double T[MAXS * MAXS];  // row-major S x S (row = test s, col = trial s')
+    int xs, vs;             // spec ids in the x / v factor
+};
+
+// one level of one factor mesh
+struct Level {
+    int64_t n = 0;
+    int m = 0;                  // lattice points per axis
+    int32_t* lat = nullptr;     // [d][n]
+    int32_t* cols = nullptr;    // [W][n] ELL pattern (column-major ELL), -1 padded
+    int32_t* pcols = nullptr;   // prolongation from level-1: [2][n]
+    double* pvals = nullptr;
+    int32_t* rcols = nullptr;   // restriction to level-1: [W][n_{l-1}]
+    double* rvals = nullptr;
+    std::vector<double*> fm;    // per spec id: [W][n], nullptr if unused
+};
+
+struct Factor {
+    int kind = SG_MESH_BOX;
+    int d = 1;
+    int nc = 2;
+    double lo[MAXD] = {0}, hi[MAXD] = {0};
+    int W = 3;                   // ELL width 2^(d+1)-1
+    std::vector<Level> lev;      // index = level (0 unused)
+    std::vector<Spec> specs;
+    int add_spec(const Spec& s);  // dedup
+};
+
+// gather entry: out[s_out] += scale * (M along dir) in[s_in]
+struct Entry {
+    const double* in;
+    const double* vals;
+    double scale;
+    int s_out, s_in;
+};
+struct EntryList {
+    int ne;
+    Entry e[MAX_ENTRIES];
+};
+struct FanoutList {
+    int no;
+    const double* vals[MAX_FANOUT];
+    double* out[MAX_FANOUT];
+};
+
+// combined (time-mixed) matrix of one group at one level
+struct CombEntry {
+    int s_out, s_in;
+    double* vals;   // [W][n] device (owned)
+};
+struct Group {                 // terms sharing one spec on the "inner" factor
+    int spec;                  // shared spec id (v-spec for lower/x-groups, x-spec for upper)
+    std::vector<int> terms;
+    // combined matrices of the OTHER factor per level: comb[level] = entries
+    std::vector<std::vector<CombEntry>> comb;
+};
+
+struct Grid {
+    int l1, l2;
+    int64_t n1, n2;
+    int64_t off1;   // offset in doubles for S=1 vectors (multiply by S for S-vectors)
+};
+
+struct Segs {  // block -> segment map for batched vector kernels over a set vector
+    int nseg;
+    int64_t off[MAX_SEG + 1];   // element offsets (for the given S)
+    int blk[MAX_SEG + 1];       // first block of each segment
+};
+
+}  // namespace sg
+
+struct sg_problem {
+    sg_config cfg;
+    cudaStream_t stream = nullptr;
+    int S = 1;
+    int F = 1;                      // finest level L-1
+    double delta = 0;
+    sg::Factor fx, fv;
+    std::vector<sg::Term> terms;
+    std::vector<sg::Group> vgroups; // grouped by v-spec; comb = x-matrices (lower part / diag v-first)
+    std::vector<sg::Group> xgroups; // grouped by x-spec; comb = v-matrices (upper part)
+    int mass_x = -1, mass_v = -1;   // spec ids of the unweighted mass
+    std::vector<sg::Grid> active, coarse;
+    bool meshes_built = false, assembled = false;
+    // workspaces
+    double* wsZ = nullptr; size_t wsZ_n = 0;      // fanout outputs / chain buffers
+    double* wsA = nullptr; size_t wsA_n = 0;      // Horner ping
+    double* wsB = nullptr; size_t wsB_n = 0;      // Horner pong
+    double* red = nullptr;                        // reduction partials
+    double* scal = nullptr;                       // per-grid scalars (BiCGStab)
+    double* hscal = nullptr;                      // pinned host copy
+    std::vector<double*> vec;                     // solver vectors
+    double* trace_dev = nullptr;
+    // instrumentation
+    int64_t n_applies = 0, dof_applied = 0, launches = 0, outer_iters = 0, inner_iters = 0;
+    bool timing = false;
+    bool verbose = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pairs;
+    double kern_ms = 0; int64_t kern_launches = 0; double kern_bytes = 0; double kern_flops = 0;
+};
+
+namespace sg {
+// mesh.cu
+int build_factor_meshes(sg_problem* P, Factor& f, int F);
+// assemble.cu
+int assemble_spec(sg_problem* P, Factor& f, int spec, int level);
+// kernels.cu launch helpers
+int launch_fanout(sg_problem* P, int dir, int W, int S, int64_t n1_in, int64_t n2_in, int64_t nrows_out,
+                  const int32_t* cols, const double* in, const FanoutList& fl);
+int launch_gather(sg_problem* P, int dir, int W, int S_out, int64_t n1_in, int64_t n2_in, int64_t nrows_out,
+                  const int32_t* cols, const EntryList& el, double* out, double beta);
+int launch_axpby(sg_problem* P, int64_t n, double a, const double* x, double b, double* y);
+int launch_copy(sg_problem* P, int64_t n, const double* x, double* y);
+int launch_zero(sg_problem* P, int64_t n, double* y);
+// solver.cu
+int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y);
+int apply_cross(sg_problem* P, const std::vector<Term>* terms_override, const double* Tb, int S_out, int S_in,
+                const double* X, double* Y);
+int64_t set_size(const sg_problem* P, int set, int S);
+}  // namespace sg

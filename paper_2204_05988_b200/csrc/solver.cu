@@ -1,0 +1,784 @@
+// Strip operator applies, cross-grid blocks, combination preconditioner,
+// Richardson strip solver and time stepping.  PAPER.md sec. 4.2-4.3, eq. (4).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "mesh_dev.cuh"
+#include "sg_internal.cuh"
+
+namespace sg {
+
+int64_t set_size(const sg_problem* P, int set, int S) {
+    const auto& gs = set == SG_SET_ACTIVE ? P->active : P->coarse;
+    int64_t n = 0;
+    for (const auto& g : gs) n += g.n1 * g.n2;
+    return n * S;
+}
+
+static inline int64_t gsize(const Grid& g) { return g.n1 * g.n2; }
+
+// ------------------------------------------------------------------ timing
+static int timed_begin(sg_problem* P, cudaEvent_t* e0) {
+    if (!P->timing) return SG_OK;
+    SG_CUDA(cudaEventCreate(e0));
+    SG_CUDA(cudaEventRecord(*e0, P->stream));
+    return SG_OK;
+}
+static int timed_end(sg_problem* P, cudaEvent_t e0, double bytes, double flops, int nl) {
+    if (!P->timing) return SG_OK;
+    cudaEvent_t e1;
+    SG_CUDA(cudaEventCreate(&e1));
+    SG_CUDA(cudaEventRecord(e1, P->stream));
+    P->ev_pairs.push_back({e0, e1});
+    P->kern_launches += nl;
+    P->kern_bytes += bytes;
+    P->kern_flops += flops;
+    return SG_OK;
+}
+
+// ------------------------------------------------ diagonal block (one grid)
+// Y = sum_t T_t (x) A_t (x) B_t X, grouped by the v-spec b:
+//   Z_b = (Id x Id x B_b) X           (fanout along v, one read of X per 4 b's)
+//   Y   = sum_b sum_{s,s'} (e_s e_s'^T (x) C_b^{ss'} (x) Id) Z_b,  C_b^{ss'} = sum_{t in b} T_t[s,s'] A_t
+// (application order of l.516-532 with S^(2) first, the intermediates stay on
+// the grid's own level because l = l').
+int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
+    const int S = P->S;
+    const int64_t n = gsize(g);
+    const Level& Lx = P->fx.lev[g.l1];
+    const Level& Lv = P->fv.lev[g.l2];
+    const int nb = (int)P->vgroups.size();
+    if ((size_t)nb * S * n > P->wsZ_n) {
+        set_error("apply_diag: workspace too small");
+        return SG_ERR_STATE;
+    }
+    cudaEvent_t e0 = nullptr;
+    SG_TRY(timed_begin(P, &e0));
+    int64_t l0 = P->launches;
+    for (int b0 = 0; b0 < nb; b0 += MAX_FANOUT) {
+        FanoutList fl;
+        fl.no = std::min(MAX_FANOUT, nb - b0);
+        for (int o = 0; o < fl.no; ++o) {
+            fl.vals[o] = Lv.fm[P->vgroups[b0 + o].spec];
+            fl.out[o] = P->wsZ + (int64_t)(b0 + o) * S * n;
+        }
+        SG_TRY(launch_fanout(P, 1, P->fv.W, S, g.n1, g.n2, g.n2, Lv.cols, X, fl));
+    }
+    EntryList el;
+    el.ne = 0;
+    double beta = 0.0;
+    int64_t nnz_x = 0;
+    for (int b = 0; b < nb; ++b) {
+        for (const auto& ce : P->vgroups[b].comb[g.l1]) {
+            if (el.ne == MAX_ENTRIES) {
+                SG_TRY(launch_gather(P, 0, P->fx.W, S, g.n1, g.n2, g.n1, Lx.cols, el, Y, beta));
+                beta = 1.0;
+                el.ne = 0;
+            }
+            el.e[el.ne++] = {P->wsZ + (int64_t)b * S * n, ce.vals, 1.0, ce.s_out, ce.s_in};
+            nnz_x++;
+        }
+    }
+    SG_TRY(launch_gather(P, 0, P->fx.W, S, g.n1, g.n2, g.n1, Lx.cols, el, Y, beta));
+    P->n_applies++;
+    P->dof_applied += S * n;
+    // algorithmic bytes: read X, write Y, factor matrices (values + pattern)
+    double bytes = 16.0 * S * n + (8.0 * nb + 4.0) * (double)(P->fv.W * g.n2) +
+                   (8.0 * nnz_x + 4.0) * (double)(P->fx.W * g.n1);
+    double flops = 2.0 * S * n * ((double)nb * P->fv.W + (double)nnz_x * P->fx.W);
+    SG_TRY(timed_end(P, e0, bytes, flops, (int)(P->launches - l0)));
+    return SG_OK;
+}
+
+// --------------------------------------------------- cross-grid full apply
+// Y_p = sum_{p'} A_{p,p'} X_{p'} over the active set (l.512-516) with the
+// cross-level factors A_{l,l'} = A_l E_{l<-l'} (l >= l') and E^T A_{l'} (l < l'),
+// which equal E_F^T A_F E_F (l.506-509) because the factor forms are
+// integrated exactly on every level.
+//  lower part (l1 >= l1'): per v-group b: Z = B_b X_{p'}, restrict in v down to
+//    the target's v-level, Horner-prolong in x up to the target's x-level, then
+//    gather with the group's combined x matrices;
+//  upper part (l1 < l1'): per x-group a symmetric with the roles of x, v swapped.
+// "mass" mode (Tb != nullptr): single term Tb (x) M^x (x) M^v, S_out x S_in.
+int apply_cross(sg_problem* P, const std::vector<Term>* /*unused*/, const double* Tb, int S_out, int S_in,
+                const double* X, double* Y) {
+    const bool mass = Tb != nullptr;
+    const auto& A = P->active;
+    const int ng = (int)A.size();
+    const int L = P->cfg.L;
+    const int Wx = P->fx.W, Wv = P->fv.W;
+    std::vector<int64_t> offIn(ng), offOut(ng);
+    for (int p = 0; p < ng; ++p) {
+        offIn[p] = A[p].off1 * S_in;
+        offOut[p] = A[p].off1 * S_out;
+    }
+    SG_TRY(launch_zero(P, set_size(P, SG_SET_ACTIVE, S_out), Y));
+    auto n1 = [&](int l) { return P->fx.lev[l].n; };
+    auto n2 = [&](int l) { return P->fv.lev[l].n; };
+    // chain buffer layout: Q[p'][k], p' = 1..ng (index p'-1), k = 0..(#targets-1)
+    std::vector<std::vector<int64_t>> qoff(ng);
+    // ---------------- lower part
+    const int nvg = mass ? 1 : (int)P->vgroups.size();
+    for (int b = 0; b < nvg; ++b) {
+        const int vspec = mass ? P->mass_v : P->vgroups[b].spec;
+        int64_t pos = 0;
+        for (int pp = 1; pp <= ng; ++pp) {
+            const int lx = pp, lv0 = L - pp;
+            qoff[pp - 1].clear();
+            for (int k = 0; k <= ng - pp; ++k) {
+                qoff[pp - 1].push_back(pos);
+                pos += (int64_t)S_in * n1(lx) * n2(lv0 - k);
+            }
+        }
+        if ((size_t)pos > P->wsZ_n) {
+            set_error("apply_cross: chain workspace too small");
+            return SG_ERR_STATE;
+        }
+        for (int pp = 1; pp <= ng; ++pp) {
+            const int lx = pp, lv0 = L - pp;
+            FanoutList fl;
+            fl.no = 1;
+            fl.vals[0] = P->fv.lev[lv0].fm[vspec];
+            fl.out[0] = P->wsZ + qoff[pp - 1][0];
+            SG_TRY(launch_fanout(P, 1, Wv, S_in, n1(lx), n2(lv0), n2(lv0), P->fv.lev[lv0].cols, X + offIn[pp - 1], fl));
+            for (int k = 1; k <= ng - pp; ++k) {
+                const int lf = lv0 - k + 1, lc = lv0 - k;
+                EntryList el;
+                el.ne = 0;
+                for (int s = 0; s < S_in; ++s)
+                    el.e[el.ne++] = {P->wsZ + qoff[pp - 1][k - 1], P->fv.lev[lf].rvals, 1.0, s, s};
+                SG_TRY(launch_gather(P, 1, Wv, S_in, n1(lx), n2(lf), n2(lc), P->fv.lev[lf].rcols, el,
+                                     P->wsZ + qoff[pp - 1][k], 0.0));
+            }
+        }
+        for (int p = 1; p <= ng; ++p) {
+            const int lv = L - p;
+            const double* acc = P->wsZ + qoff[0][p - 1];   // Q_{1,p-1} at (1, lv)
+            double* bufs[2] = {P->wsA, P->wsB};
+            int cur = 0;
+            for (int m = 2; m <= p; ++m) {
+                double* dst = bufs[cur];
+                SG_TRY(launch_copy(P, (int64_t)S_in * n1(m) * n2(lv), P->wsZ + qoff[m - 1][p - m], dst));
+                EntryList el;
+                el.ne = 0;
+                for (int s = 0; s < S_in; ++s) el.e[el.ne++] = {acc, P->fx.lev[m].pvals, 1.0, s, s};
+                SG_TRY(launch_gather(P, 0, 2, S_in, n1(m - 1), n2(lv), n1(m), P->fx.lev[m].pcols, el, dst, 1.0));
+                acc = dst;
+                cur ^= 1;
+            }
+            EntryList el;
+            el.ne = 0;
+            if (mass) {
+                for (int s = 0; s < S_out; ++s)
+                    for (int sp = 0; sp < S_in; ++sp)
+                        if (Tb[s * S_in + sp] != 0.0)
+                            el.e[el.ne++] = {acc, P->fx.lev[p].fm[P->mass_x], Tb[s * S_in + sp], s, sp};
+            } else {
+                for (const auto& ce : P->vgroups[b].comb[p]) el.e[el.ne++] = {acc, ce.vals, 1.0, ce.s_out, ce.s_in};
+            }
+            if (el.ne) SG_TRY(launch_gather(P, 0, Wx, S_out, n1(p), n2(lv), n1(p), P->fx.lev[p].cols, el,
+                                            Y + offOut[p - 1], 1.0));
+        }
+    }
+    // ---------------- upper part (targets p < sources p')
+    if (ng >= 2) {
+        const int nxg = mass ? 1 : (int)P->xgroups.size();
+        for (int a = 0; a < nxg; ++a) {
+            const int xspec = mass ? P->mass_x : P->xgroups[a].spec;
+            int64_t pos = 0;
+            for (int pp = 2; pp <= ng; ++pp) {
+                const int lv = L - pp;
+                qoff[pp - 1].clear();
+                for (int k = 0; k <= pp - 1; ++k) {       // k: x-level pp-k
+                    qoff[pp - 1].push_back(pos);
+                    pos += (int64_t)S_in * n1(pp - k) * n2(lv);
+                }
+            }
+            if ((size_t)pos > P->wsZ_n) {
+                set_error("apply_cross: chain workspace too small (upper)");
+                return SG_ERR_STATE;
+            }
+            for (int pp = 2; pp <= ng; ++pp) {
+                const int lv = L - pp;
+                FanoutList fl;
+                fl.no = 1;
+                fl.vals[0] = P->fx.lev[pp].fm[xspec];
+                fl.out[0] = P->wsZ + qoff[pp - 1][0];
+                SG_TRY(launch_fanout(P, 0, Wx, S_in, n1(pp), n2(lv), n1(pp), P->fx.lev[pp].cols, X + offIn[pp - 1], fl));
+                for (int k = 1; k <= pp - 1; ++k) {
+                    const int lf = pp - k + 1, lc = pp - k;
+                    EntryList el;
+                    el.ne = 0;
+                    for (int s = 0; s < S_in; ++s)
+                        el.e[el.ne++] = {P->wsZ + qoff[pp - 1][k - 1], P->fx.lev[lf].rvals, 1.0, s, s};
+                    SG_TRY(launch_gather(P, 0, Wx, S_in, n1(lf), n2(lv), n1(lc), P->fx.lev[lf].rcols, el,
+                                         P->wsZ + qoff[pp - 1][k], 0.0));
+                }
+            }
+            for (int p = 1; p <= ng - 1; ++p) {
+                const int lvt = L - p;
+                // Horner in v: start at source p' = ng (v-level L-ng), end at v-level L-p
+                const double* acc = P->wsZ + qoff[ng - 1][ng - p];
+                int accl = L - ng;
+                double* bufs[2] = {P->wsA, P->wsB};
+                int cur = 0;
+                for (int pp = ng - 1; pp >= p + 1; --pp) {
+                    const int lvn = L - pp;   // = accl + 1
+                    double* dst = bufs[cur];
+                    SG_TRY(launch_copy(P, (int64_t)S_in * n1(p) * n2(lvn), P->wsZ + qoff[pp - 1][pp - p], dst));
+                    EntryList el;
+                    el.ne = 0;
+                    for (int s = 0; s < S_in; ++s) el.e[el.ne++] = {acc, P->fv.lev[lvn].pvals, 1.0, s, s};
+                    SG_TRY(launch_gather(P, 1, 2, S_in, n1(p), n2(accl), n2(lvn), P->fv.lev[lvn].pcols, el, dst, 1.0));
+                    acc = dst;
+                    accl = lvn;
+                    cur ^= 1;
+                }
+                {
+                    // final prolongation to the target v-level
+                    double* dst = bufs[cur];
+                    EntryList el;
+                    el.ne = 0;
+                    for (int s = 0; s < S_in; ++s) el.e[el.ne++] = {acc, P->fv.lev[lvt].pvals, 1.0, s, s};
+                    SG_TRY(launch_gather(P, 1, 2, S_in, n1(p), n2(accl), n2(lvt), P->fv.lev[lvt].pcols, el, dst, 0.0));
+                    acc = dst;
+                }
+                EntryList el;
+                el.ne = 0;
+                if (mass) {
+                    for (int s = 0; s < S_out; ++s)
+                        for (int sp = 0; sp < S_in; ++sp)
+                            if (Tb[s * S_in + sp] != 0.0)
+                                el.e[el.ne++] = {acc, P->fv.lev[lvt].fm[P->mass_v], Tb[s * S_in + sp], s, sp};
+                } else {
+                    for (const auto& ce : P->xgroups[a].comb[lvt]) el.e[el.ne++] = {acc, ce.vals, 1.0, ce.s_out, ce.s_in};
+                }
+                if (el.ne) SG_TRY(launch_gather(P, 1, Wv, S_out, n1(p), n2(lvt), n2(lvt), P->fv.lev[lvt].cols, el,
+                                                Y + offOut[p - 1], 1.0));
+            }
+        }
+    }
+    return SG_OK;
+}
+
+// ------------------------------------------------------- segmented vectors
+struct SegTab {
+    int nseg;
+    int64_t off[MAX_SEG + 1];
+    int blk[MAX_SEG + 1];
+};
+constexpr int SEG_CHUNK = 2048;
+
+static SegTab make_segs(const std::vector<int64_t>& offs) {   // offs: nseg+1 element offsets
+    SegTab t;
+    t.nseg = (int)offs.size() - 1;
+    int b = 0;
+    for (int i = 0; i <= t.nseg; ++i) {
+        t.off[i] = offs[i];
+        t.blk[i] = b;
+        if (i < t.nseg) b += (int)((offs[i + 1] - offs[i] + SEG_CHUNK - 1) / SEG_CHUNK);
+    }
+    return t;
+}
+
+__device__ inline int seg_of(const SegTab& t, int blk) {
+    int g = 0;
+    while (g + 1 < t.nseg && t.blk[g + 1] <= blk) ++g;
+    return g;
+}
+
+// per-grid scalars: [0] rho [1] alpha [2] omega [3] bnorm2 [4] rnorm2 [5] conv [6] r0v [7] ts [8] tt [9] rr
+constexpr int NSC = 10;
+
+// partial[blk*K + j] = sum over the block's chunk of a_j * b_j
+template <int K>
+__global__ void k_seg_dot(SegTab t, const double* a0, const double* b0, const double* a1, const double* b1,
+                          double* partial, const double* a2 = nullptr, const double* b2 = nullptr) {
+    __shared__ double sh[K][8];
+    const int g = seg_of(t, blockIdx.x);
+    const int64_t lo = t.off[g] + (int64_t)(blockIdx.x - t.blk[g]) * SEG_CHUNK;
+    const int64_t hi = min(lo + SEG_CHUNK, t.off[g + 1]);
+    double s[K];
+    for (int j = 0; j < K; ++j) s[j] = 0.0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        s[0] += a0[i] * b0[i];
+        if (K > 1) s[1] += a1[i] * b1[i];
+        if (K > 2) s[2] += a2[i] * b2[i];
+    }
+    for (int j = 0; j < K; ++j) {
+        double v = s[j];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0) sh[j][threadIdx.x >> 5] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < K) {
+        double v = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += sh[threadIdx.x][w];
+        partial[(int64_t)blockIdx.x * K + threadIdx.x] = v;
+    }
+}
+
+// reduce partials of each segment into scal[g*NSC + slot_j], then apply `op`
+// op 0: init (rho = bnorm2 = rr; conv if 0)
+// op 1: alpha = rho / r0v
+// op 2: omega = ts / tt
+// op 3: rho_new, rnorm2 -> beta, convergence
+__global__ void k_seg_finalize(SegTab t, int K, const double* partial, double* scal, int s0, int s1, int op,
+                               double tol2) {
+    const int g = blockIdx.x;
+    if (g >= t.nseg) return;
+    __shared__ double sh[3][32];
+    double v[3] = {0.0, 0.0, 0.0};
+    for (int b = t.blk[g] + threadIdx.x; b < t.blk[g + 1]; b += blockDim.x)
+        for (int j = 0; j < K; ++j) v[j] += partial[(int64_t)b * K + j];
+    for (int j = 0; j < K; ++j) {
+        double x = v[j];
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if ((threadIdx.x & 31) == 0) sh[j][threadIdx.x >> 5] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    double r[3] = {0.0, 0.0, 0.0};
+    for (int j = 0; j < K; ++j)
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r[j] += sh[j][w];
+    double* sc = scal + g * NSC;
+    if (op < 0) {
+        sc[s0] = r[0];
+        return;
+    }
+    if (op == 0) {
+        sc[0] = r[0];
+        sc[3] = r[0];
+        sc[4] = r[0];
+        sc[5] = (r[0] == 0.0) ? 1.0 : 0.0;
+        sc[1] = 0.0;
+        sc[2] = 0.0;
+        sc[6] = 0.0;
+        return;
+    }
+    if (sc[5] != 0.0) return;   // converged grid: scalars frozen
+    if (op == 1) {              // alpha = rho / (r0.v)
+        const double a = sc[0] / r[0];
+        if (r[0] == 0.0 || !isfinite(a)) {
+            sc[1] = 0.0;
+            sc[2] = 0.0;
+            sc[5] = 2.0;        // breakdown
+        } else {
+            sc[1] = a;
+        }
+    } else if (op == 2) {       // r = (t.s, t.t, s.s): omega, or converge at the half step
+        if (r[2] <= tol2 * sc[3]) {
+            sc[2] = 0.0;        // x += alpha p, r = s
+            sc[7] = 1.0;        // converge after the update
+        } else {
+            const double om = r[0] / r[1];
+            sc[2] = (r[1] > 0.0 && isfinite(om)) ? om : 0.0;
+            sc[7] = 0.0;
+        }
+    } else if (op == 3) {       // r = (r0.r, r.r)
+        const double rho_new = r[0];
+        sc[4] = r[1];
+        double beta = 0.0;
+        if (sc[0] != 0.0 && sc[2] != 0.0) beta = (rho_new / sc[0]) * (sc[1] / sc[2]);
+        sc[0] = rho_new;
+        sc[6] = isfinite(beta) ? beta : 0.0;
+        if (sc[7] != 0.0 || r[1] <= tol2 * sc[3]) sc[5] = 1.0;
+        else if (rho_new == 0.0 || !isfinite(rho_new) || !isfinite(r[1]) || sc[2] == 0.0) sc[5] = 2.0;
+    }
+}
+
+// s = r - alpha v
+__global__ void k_bicg_s(SegTab t, const double* scal, const double* r, const double* v, double* s) {
+    const int g = seg_of(t, blockIdx.x);
+    const double* sc = scal + g * NSC;
+    if (sc[5] != 0.0) return;
+    const double al = sc[1];
+    const int64_t lo = t.off[g] + (int64_t)(blockIdx.x - t.blk[g]) * SEG_CHUNK;
+    const int64_t hi = min(lo + SEG_CHUNK, t.off[g + 1]);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s[i] = r[i] - al * v[i];
+}
+
+// x += alpha p + omega s ; r = s - omega t ; partial dots (r0.r, r.r)
+__global__ void k_bicg_xr(SegTab tb, const double* scal, double* x, double* r, const double* p, const double* s,
+                          const double* t, const double* r0, double* partial) {
+    __shared__ double sh[2][8];
+    const int g = seg_of(tb, blockIdx.x);
+    const double* sc = scal + g * NSC;
+    const bool active = sc[5] == 0.0;
+    const double al = sc[1], om = sc[2];
+    const int64_t lo = tb.off[g] + (int64_t)(blockIdx.x - tb.blk[g]) * SEG_CHUNK;
+    const int64_t hi = min(lo + SEG_CHUNK, tb.off[g + 1]);
+    double a0 = 0.0, a1 = 0.0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        double ri = r[i];
+        if (active) {
+            x[i] += al * p[i] + om * s[i];
+            ri = s[i] - om * t[i];
+            r[i] = ri;
+        }
+        a0 += r0[i] * ri;
+        a1 += ri * ri;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+        a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        sh[0][threadIdx.x >> 5] = a0;
+        sh[1][threadIdx.x >> 5] = a1;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        double v = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += sh[threadIdx.x][w];
+        partial[(int64_t)blockIdx.x * 2 + threadIdx.x] = v;
+    }
+}
+
+// p = r + beta (p - omega v)
+__global__ void k_bicg_p(SegTab t, const double* scal, double* p, const double* r, const double* v) {
+    const int g = seg_of(t, blockIdx.x);
+    const double* sc = scal + g * NSC;
+    if (sc[5] != 0.0) return;
+    const double be = sc[6], om = sc[2];
+    const int64_t lo = t.off[g] + (int64_t)(blockIdx.x - t.blk[g]) * SEG_CHUNK;
+    const int64_t hi = min(lo + SEG_CHUNK, t.off[g + 1]);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) p[i] = r[i] + be * (p[i] - om * v[i]);
+}
+
+// batched BiCGStab on the grids `gr` (block solves of eq. (15)); b, x concatenated in order of gr
+static int bicgstab(sg_problem* P, const std::vector<const Grid*>& gr, const double* b, double* x, double rtol,
+                    int maxit) {
+    const int S = P->S;
+    std::vector<int64_t> offs(1, 0);
+    for (auto* g : gr) offs.push_back(offs.back() + S * gsize(*g));
+    const int64_t N = offs.back();
+    SegTab t = make_segs(offs);
+    const int nblk = t.blk[t.nseg];
+    double *r = P->vec[0], *r0 = P->vec[1], *p = P->vec[2], *v = P->vec[3], *s = P->vec[4], *tt = P->vec[5];
+    SG_TRY(launch_zero(P, N, x));
+    SG_TRY(launch_copy(P, N, b, r));
+    SG_TRY(launch_copy(P, N, b, r0));
+    SG_TRY(launch_copy(P, N, b, p));
+    k_seg_dot<1><<<nblk, 256, 0, P->stream>>>(t, b, b, nullptr, nullptr, P->red);
+    k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 1, P->red, P->scal, 9, 9, 0, 0.0);
+    P->launches += 2;
+    const double tol2 = rtol * rtol;
+    std::vector<char> conv(gr.size(), 0);
+    for (int it = 0; it < maxit; ++it) {
+        // v = A p
+        for (size_t i = 0; i < gr.size(); ++i)
+            if (!conv[i]) SG_TRY(apply_diag(P, *gr[i], p + offs[i], v + offs[i]));
+        k_seg_dot<1><<<nblk, 256, 0, P->stream>>>(t, r0, v, nullptr, nullptr, P->red);
+        k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 1, P->red, P->scal, 6, 6, 1, tol2);
+        k_bicg_s<<<nblk, 256, 0, P->stream>>>(t, P->scal, r, v, s);
+        for (size_t i = 0; i < gr.size(); ++i)
+            if (!conv[i]) SG_TRY(apply_diag(P, *gr[i], s + offs[i], tt + offs[i]));
+        k_seg_dot<3><<<nblk, 256, 0, P->stream>>>(t, tt, s, tt, tt, P->red, s, s);
+        k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 3, P->red, P->scal, 7, 8, 2, tol2);
+        k_bicg_xr<<<nblk, 256, 0, P->stream>>>(t, P->scal, x, r, p, s, tt, r0, P->red);
+        k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 2, P->red, P->scal, 0, 4, 3, tol2);
+        k_bicg_p<<<nblk, 256, 0, P->stream>>>(t, P->scal, p, r, v);
+        P->launches += 8;
+        SG_CUDA(cudaGetLastError());
+        P->inner_iters++;
+        SG_CUDA(cudaMemcpyAsync(P->hscal, P->scal, sizeof(double) * NSC * gr.size(), cudaMemcpyDeviceToHost,
+                                P->stream));
+        SG_CUDA(cudaStreamSynchronize(P->stream));
+        bool all = true;
+        for (size_t i = 0; i < gr.size(); ++i) {
+            conv[i] = P->hscal[i * NSC + 5] != 0.0;
+            all &= (bool)conv[i];
+        }
+        if (all) break;
+    }
+    return SG_OK;
+}
+
+// ------------------------------------------------------------ combination
+// du_p = dhat_p - (E^(1)_{l1<-l1-1} x Id) dhat_{(l1-1,l2)}  (l.557-565)
+int combine(sg_problem* P, int S, const double* dhat_a, const double* dhat_c, double* du) {
+    const auto& A = P->active;
+    for (size_t p = 0; p < A.size(); ++p) {
+        const Grid& g = A[p];
+        SG_TRY(launch_copy(P, S * gsize(g), dhat_a + g.off1 * S, du + g.off1 * S));
+        if (g.l1 > 1) {
+            const Grid& c = P->coarse[g.l1 - 2];   // (l1-1, l2)
+            EntryList el;
+            el.ne = 0;
+            for (int s = 0; s < S; ++s)
+                el.e[el.ne++] = {dhat_c + c.off1 * S, P->fx.lev[g.l1].pvals, -1.0, s, s};
+            SG_TRY(launch_gather(P, 0, 2, S, c.n1, c.n2, g.n1, P->fx.lev[g.l1].pcols, el, du + g.off1 * S, 1.0));
+        }
+    }
+    return SG_OK;
+}
+
+static double host_dot(sg_problem* P, int64_t n, const double* a, const double* b, int* err) {
+    std::vector<int64_t> offs = {0, n};
+    SegTab t = make_segs(offs);
+    k_seg_dot<1><<<t.blk[1], 256, 0, P->stream>>>(t, a, b, nullptr, nullptr, P->red);
+    // finalize into slot 9 of a scratch segment placed after the BiCGStab scalars
+    double* sc = P->scal + NSC * MAX_SEG;
+    k_seg_finalize<<<1, 256, 0, P->stream>>>(t, 1, P->red, sc, 9, 9, -1, 0.0);
+    P->launches += 2;
+    double h = 0.0;
+    if (cudaMemcpyAsync(&h, sc + 9, sizeof(double), cudaMemcpyDeviceToHost, P->stream) != cudaSuccess ||
+        cudaStreamSynchronize(P->stream) != cudaSuccess)
+        *err = SG_ERR_CUDA;
+    return h;
+}
+
+// ------------------------------------------------------------ Richardson
+int solve_strip(sg_problem* P, const double* b, double* u, double rtol, double inner_rtol, int max_iter, int* iters,
+                double* last) {
+    const int S = P->S;
+    const int64_t Na = set_size(P, SG_SET_ACTIVE, S), Nc = set_size(P, SG_SET_COARSE, S);
+    double* r = P->vec[6];
+    double* rhs = P->vec[7];      // [active | coarse]
+    double* dhat = P->vec[8];     // [active | coarse]
+    double* du = P->vec[9];
+    double* Mw = P->vec[10];
+    std::vector<const Grid*> gr;
+    for (auto& g : P->active) gr.push_back(&g);
+    for (auto& g : P->coarse) gr.push_back(&g);
+    double Mt[4] = {0, 0, 0, 0};
+    Mt[0] = P->cfg.tau;
+    if (S == 2) Mt[3] = P->cfg.tau / 3.0;
+    int it = 0;
+    double nd = 0.0;
+    for (it = 1; it <= max_iter; ++it) {
+        P->outer_iters++;
+        SG_TRY(apply_cross(P, nullptr, nullptr, S, S, u, r));                 // r = A u
+        SG_TRY(launch_axpby(P, Na, -1.0, b, 1.0, r));                        // r -= b
+        SG_TRY(launch_copy(P, Na, r, rhs));
+        for (size_t c = 0; c < P->coarse.size(); ++c) {                       // (Id x E^T x Id) r, l.552
+            const Grid& cg = P->coarse[c];
+            const Grid& src = P->active[cg.l1];                               // (c1+1, c2)
+            EntryList el;
+            el.ne = 0;
+            for (int s = 0; s < S; ++s) el.e[el.ne++] = {r + src.off1 * S, P->fx.lev[src.l1].rvals, 1.0, s, s};
+            SG_TRY(launch_gather(P, 0, P->fx.W, S, src.n1, src.n2, cg.n1, P->fx.lev[src.l1].rcols, el,
+                                 rhs + Na + cg.off1 * S, 0.0));
+        }
+        SG_TRY(bicgstab(P, gr, rhs, dhat, inner_rtol, 500));
+        SG_TRY(combine(P, S, dhat, dhat + Na, du));
+        SG_TRY(launch_axpby(P, Na, -1.0, du, 1.0, u));
+        int err = SG_OK;
+        SG_TRY(apply_cross(P, nullptr, Mt, S, S, du, Mw));
+        double nd2 = host_dot(P, Na, du, Mw, &err);
+        SG_TRY(apply_cross(P, nullptr, Mt, S, S, u, Mw));
+        double nu2 = host_dot(P, Na, u, Mw, &err);
+        if (err) return err;
+        nd = std::sqrt(std::max(nd2, 0.0));
+        double nu = std::sqrt(std::max(nu2, 0.0));
+        if (P->verbose) fprintf(stderr, "[sg] richardson it %d |du| %.3e |u| %.3e inner %lld\n", it, nd, nu,
+                                (long long)P->inner_iters);
+        if (!std::isfinite(nd2) || !std::isfinite(nu2)) {
+            set_error("solve_strip: non-finite update (inner solver breakdown)");
+            return SG_ERR_STATE;
+        }
+        if (nd <= rtol * nu || nd == 0.0) break;
+    }
+    if (iters) *iters = std::min(it, max_iter);
+    if (last) *last = nd;
+    (void)Nc;
+    return SG_OK;
+}
+
+// ------------------------------------------------------- data (u0, inflow)
+__global__ void k_gauss_nodes(int64_t n, int d, const int32_t* lat, double lo0, double lo1, double lo2, double h0,
+                              double h1, double h2, double c0, double c1, double c2, double w, double scale,
+                              double shift0, double shift1, double shift2, double* out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double lo[3] = {lo0, lo1, lo2}, h[3] = {h0, h1, h2}, c[3] = {c0, c1, c2}, sh[3] = {shift0, shift1, shift2};
+    double r2 = 0.0;
+    for (int k = 0; k < d; ++k) {
+        double y = lo[k] + h[k] * lat[k * n + i] - sh[k] - c[k];
+        r2 += y * y;
+    }
+    out[i] = scale * exp(-r2 / w);
+}
+
+// out[k][m] (+)= coef * gx[k] * gv[m]
+__global__ void k_outer(int64_t n1, int64_t n2, double coef, const double* gx, const double* gv, double* out,
+                        int accumulate) {
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n1 * n2) return;
+    int64_t k = t / n2, m = t - k * n2;
+    double v = coef * gx[k] * gv[m];
+    out[t] = accumulate ? out[t] + v : v;
+}
+
+// y[i*sy] += a * x[i*sx]
+__global__ void k_axpy_strided(int64_t n, double a, const double* x, int64_t sx, double* y, int64_t sy) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) y[i * sy] += a * x[i * sx];
+}
+
+static int gauss_on_level(sg_problem* P, Factor& f, int l, const double* c, double w, double s, const double* shift,
+                          double* out) {
+    Level& L = f.lev[l];
+    const int cells = f.nc << (l - 1);
+    double h[3] = {0, 0, 0}, lo[3] = {0, 0, 0}, sh[3] = {0, 0, 0}, cc[3] = {0, 0, 0};
+    for (int i = 0; i < f.d; ++i) {
+        h[i] = (f.hi[i] - f.lo[i]) / cells;
+        lo[i] = f.lo[i];
+        cc[i] = c[i];
+        if (shift) sh[i] = shift[i];
+    }
+    k_gauss_nodes<<<(int)((L.n + 255) / 256), 256, 0, P->stream>>>(L.n, f.d, L.lat, lo[0], lo[1], lo[2], h[0], h[1],
+                                                                  h[2], cc[0], cc[1], cc[2], w, s, sh[0], sh[1],
+                                                                  sh[2], out);
+    P->launches++;
+    SG_CUDA(cudaGetLastError());
+    return SG_OK;
+}
+
+// U_0^- = combination of nodal interpolants of u0 (reading R8)
+int interp_u0(sg_problem* P, double* u) {
+    double* va = P->vec[7];
+    const int64_t Na = set_size(P, SG_SET_ACTIVE, 1);
+    double* gx = P->vec[10];
+    double* gv = gx + (P->fx.lev[P->F].n + 16);
+    for (int set = 0; set < 2; ++set) {
+        const auto& gs = set == 0 ? P->active : P->coarse;
+        for (const auto& g : gs) {
+            double* dst = va + (set == 0 ? 0 : Na) + g.off1;
+            for (int r = 0; r < P->cfg.nu0; ++r) {
+                const sg_gauss_term& tm = P->cfg.u0[r];
+                SG_TRY(gauss_on_level(P, P->fx, g.l1, tm.xc, tm.xw, tm.xs, nullptr, gx));
+                SG_TRY(gauss_on_level(P, P->fv, g.l2, tm.vc, tm.vw, tm.vs, nullptr, gv));
+                int64_t n = g.n1 * g.n2;
+                k_outer<<<(int)((n + 255) / 256), 256, 0, P->stream>>>(g.n1, g.n2, tm.coef, gx, gv, dst, r > 0);
+                P->launches++;
+            }
+        }
+    }
+    SG_CUDA(cudaGetLastError());
+    return combine(P, 1, va, va + Na, u);
+}
+
+// inflow load for g = u0(r - beta t), constant beta, d = 1 (reading R9)
+static int inflow_load(sg_problem* P, double t0, double* b) {
+    const int S = P->S, F = P->F;
+    const sg_config& c = P->cfg;
+    double beta[2] = {0, 0};
+    for (int r = 0; r < c.nbeta; ++r) beta[c.beta[r].axis] += c.beta[r].a[0] * c.beta[r].b[0];
+    const double r6 = std::sqrt(6.0 / 5.0);
+    const double xa = std::sqrt(3.0 / 7.0 - 2.0 / 7.0 * r6), xb = std::sqrt(3.0 / 7.0 + 2.0 / 7.0 * r6);
+    const double wa = (18.0 + std::sqrt(30.0)) / 36.0, wb = (18.0 - std::sqrt(30.0)) / 36.0;
+    const double gx_[4] = {-xb, -xa, xa, xb}, gw_[4] = {wb, wa, wa, wb};
+    double* tmp = P->vec[10];
+    const int64_t nF = std::max(P->fx.lev[F].n, P->fv.lev[F].n) + 16;
+    double* gF = tmp;
+    double* lF = tmp + nF;
+    double* chainA = tmp + 2 * nF;
+    double* chainB = tmp + 3 * nF;
+    for (int mu = 0; mu < 4; ++mu) {
+        const double t = t0 + c.tau * (gx_[mu] + 1.0) / 2.0;
+        const double wt = gw_[mu] * c.tau / 2.0;
+        double eta[2] = {1.0, gx_[mu]};
+        for (int face = 0; face < 2; ++face) {          // 0: x faces, 1: v faces
+            Factor& fb = face == 0 ? P->fv : P->fx;     // factor along the face
+            Factor& fn = face == 0 ? P->fx : P->fv;     // factor normal to the face
+            const double bn_axis = beta[face];
+            for (int sface = -1; sface <= 1; sface += 2) {
+                const double bn = sface * bn_axis;
+                if (!(bn < 0.0)) continue;
+                const double ypt = sface < 0 ? fn.lo[0] : fn.hi[0];
+                for (int r = 0; r < c.nu0; ++r) {
+                    const sg_gauss_term& tm = c.u0[r];
+                    // normal factor value at the face point, shifted
+                    const double* cn = face == 0 ? tm.xc : tm.vc;
+                    const double wn = face == 0 ? tm.xw : tm.vw, sn = face == 0 ? tm.xs : tm.vs;
+                    const double yy = ypt - bn_axis * t - cn[0];
+                    const double gnorm = sn * std::exp(-yy * yy / wn);
+                    const double* cb = face == 0 ? tm.vc : tm.xc;
+                    const double wb2 = face == 0 ? tm.vw : tm.xw, sb = face == 0 ? tm.vs : tm.xs;
+                    double shift[3] = {beta[1 - face] * t, 0, 0};
+                    SG_TRY(gauss_on_level(P, fb, F, cb, wb2, sb, shift, gF));
+                    // lF = M_F gF
+                    EntryList el;
+                    el.ne = 1;
+                    const int mspec = face == 0 ? P->mass_v : P->mass_x;
+                    el.e[0] = {gF, fb.lev[F].fm[mspec], 1.0, 0, 0};
+                    SG_TRY(launch_gather(P, 1, fb.W, 1, 1, fb.lev[F].n, fb.lev[F].n, fb.lev[F].cols, el, lF, 0.0));
+                    // per active grid: restrict to the grid's level along the face factor
+                    for (const auto& g : P->active) {
+                        const int lb = face == 0 ? g.l2 : g.l1;
+                        const double* cur = lF;
+                        double* bufs[2] = {chainA, chainB};
+                        int k = 0;
+                        for (int l = F; l > lb; --l) {
+                            EntryList e2;
+                            e2.ne = 1;
+                            e2.e[0] = {cur, fb.lev[l].rvals, 1.0, 0, 0};
+                            SG_TRY(launch_gather(P, 1, fb.W, 1, 1, fb.lev[l].n, fb.lev[l - 1].n, fb.lev[l].rcols, e2,
+                                                 bufs[k], 0.0));
+                            cur = bufs[k];
+                            k ^= 1;
+                        }
+                        const int64_t nb_ = fb.lev[lb].n;
+                        const int64_t node = sface < 0 ? 0 : (face == 0 ? g.n1 - 1 : g.n2 - 1);
+                        for (int s = 0; s < S; ++s) {
+                            double a = -bn * wt * eta[s] * c.u0[r].coef * gnorm;
+                            double* dst = b + g.off1 * S + (int64_t)s * g.n1 * g.n2;
+                            if (face == 0)
+                                k_axpy_strided<<<(int)((nb_ + 255) / 256), 256, 0, P->stream>>>(
+                                    nb_, a, cur, 1, dst + node * g.n2, 1);
+                            else
+                                k_axpy_strided<<<(int)((nb_ + 255) / 256), 256, 0, P->stream>>>(
+                                    nb_, a, cur, 1, dst + node, g.n2);
+                            P->launches++;
+                        }
+                    }
+                }
+            }
+        }
+    }
+    SG_CUDA(cudaGetLastError());
+    return SG_OK;
+}
+
+// b = eta(t_{j-1}^+) (x) M_cross trace + inflow
+int rhs(sg_problem* P, int j, const double* trace, double* b) {
+    const int S = P->S;
+    double em[2] = {1.0, -1.0};
+    SG_TRY(apply_cross(P, nullptr, em, S, 1, trace, b));
+    if (P->cfg.inflow) SG_TRY(inflow_load(P, (j - 1) * P->cfg.tau, b));
+    return SG_OK;
+}
+
+// trace = sum_s eta_s(t_j^-) u_s  (eta(1) = 1 for Legendre)
+int trace_of(sg_problem* P, const double* u, double* tr) {
+    const int S = P->S;
+    for (const auto& g : P->active) {
+        const int64_t n = gsize(g);
+        SG_TRY(launch_copy(P, n, u + g.off1 * S, tr + g.off1));
+        for (int s = 1; s < S; ++s) SG_TRY(launch_axpby(P, n, 1.0, u + g.off1 * S + s * n, 1.0, tr + g.off1));
+    }
+    return SG_OK;
+}
+
+int step(sg_problem* P, int j0, int nsteps, double* trace_dev, double rtol, double inner_rtol) {
+    const int S = P->S;
+    const int64_t Na = set_size(P, SG_SET_ACTIVE, S);
+    double* b = P->vec[11];
+    double* u = P->vec[12];
+    for (int j = j0; j < j0 + nsteps; ++j) {
+        SG_TRY(rhs(P, j, trace_dev, b));
+        SG_TRY(launch_zero(P, Na, u));
+        int it = 0;
+        double last = 0;
+        SG_TRY(solve_strip(P, b, u, rtol, inner_rtol, 200, &it, &last));
+        SG_TRY(trace_of(P, u, trace_dev));
+    }
+    return SG_OK;
+}
+
+}  // namespace sg

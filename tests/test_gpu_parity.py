@@ -1,0 +1,249 @@
+"""GPU parity: the CUDA path (libsg.so through the C ABI) vs the oracle.
+
+Bars: bit-exact for meshes / patterns / transfer indices; fp64 relative
+max-norm 1e-12 per operator apply (BASELINE north_star); 1e-9 relative on the
+solution function after stepping.  Sizes span several tiles and ragged tails.
+"""
+import numpy as np
+import pytest
+
+from sginputs import CONFIG_ORDER, get_config
+from tests.gpu_helpers import SET_ACTIVE, SET_COARSE, from_blocks, oracle_spec, relmax, to_blocks
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+SMALL = {"c0_2d_const": 6, "c1_2d_rot": 5, "c2_4d_stream": 4, "c3_4d_lshape": 4, "c4_6d_stream": 3}
+
+_cache = {}
+
+
+def pair(name, L=None):
+    """(gpu Problem, oracle SGProblem) for a config at a small level."""
+    L = SMALL[name] if L is None else L
+    key = (name, L)
+    if key not in _cache:
+        from oracle.sgrid import SGProblem
+        from paper_2204_05988_b200 import Problem
+        cfg = get_config(name, L=L)
+        _cache[key] = (Problem(cfg), SGProblem(cfg))
+    return _cache[key]
+
+
+@pytest.mark.parametrize("name", CONFIG_ORDER)
+def test_meshes_bit_exact(name):
+    from oracle.mesh import pattern_ell
+    g, o = pair(name)
+    for fac, H in ((0, o.Hx), (1, o.Hv)):
+        for l in range(1, o.F + 1):
+            lat, cols = g.mesh_export(fac, l)
+            m = H.meshes[l]
+            assert np.array_equal(lat, m.lattice.astype(np.int32)), (fac, l)
+            assert np.array_equal(cols, pattern_ell(m, cols.shape[1])), (fac, l)
+            if l >= 2:
+                pc, pv, rc, rv = g.transfer_export(fac, l)
+                E = H.E1[l - 1]
+                Et = E.T.tocsr()
+                for i in range(m.n):
+                    cc = E.indices[E.indptr[i]:E.indptr[i + 1]]
+                    vv = E.data[E.indptr[i]:E.indptr[i + 1]]
+                    assert np.array_equal(pc[i][pc[i] >= 0], cc) and np.array_equal(pv[i][pc[i] >= 0], vv)
+                for i in range(H.n(l - 1)):
+                    cc = Et.indices[Et.indptr[i]:Et.indptr[i + 1]]
+                    vv = Et.data[Et.indptr[i]:Et.indptr[i + 1]]
+                    assert np.array_equal(rc[i][rc[i] >= 0], cc) and np.array_equal(rv[i][rc[i] >= 0], vv)
+
+
+@pytest.mark.parametrize("name", CONFIG_ORDER)
+def test_factor_matrices(name):
+    from oracle.fem import assemble
+    g, o = pair(name)
+    d = o.d
+    for fac, H in ((0, o.Hx), (1, o.Hv)):
+        for sp in range(g.num_specs(fac)):
+            spec = oracle_spec(g.spec_info(fac, sp), d)
+            for l in range(1, o.F + 1):
+                vals = g.factor_export(fac, sp, l)
+                A = assemble(H.meshes[l], spec)
+                _, cols = g.mesh_export(fac, l)
+                ref = np.zeros_like(vals)
+                for i in range(A.shape[0]):
+                    k = cols[i] >= 0
+                    ref[i, k] = A[i, cols[i][k]].toarray().ravel()
+                scale = max(np.abs(ref).max(), 1e-300)
+                assert np.abs(vals - ref).max() <= 1e-13 * scale, (fac, sp, l, spec)
+
+
+@pytest.mark.parametrize("name", CONFIG_ORDER)
+def test_term_expansion_same_operator(name):
+    """sum_t T_t (x) X_t (x) V_t from the GPU term list == the oracle's (dense, one grid)."""
+    from oracle.fem import assemble
+    g, o = pair(name)
+    l = o.active[len(o.active) // 2]
+    mx, mv = o.Hx.meshes[l[0]], o.Hv.meshes[l[1]]
+    D1 = 0
+    for T, xs, vs in g.terms():
+        X = assemble(mx, oracle_spec(g.spec_info(0, xs), o.d)).toarray()
+        V = assemble(mv, oracle_spec(g.spec_info(1, vs), o.d)).toarray()
+        D1 = D1 + np.kron(T, np.kron(X, V))
+    D2 = o.block_matrix(o.terms, l, l).toarray()
+    assert relmax(D1, D2) <= 1e-13
+
+
+@pytest.mark.parametrize("name", CONFIG_ORDER)
+def test_apply_strip_operator(name):
+    """Per-grid strip operator (the hot path) on every active and coarse grid."""
+    g, o = pair(name)
+    rng = np.random.default_rng(0)
+    for set_, grids in ((SET_ACTIVE, o.active), (SET_COARSE, o.coarse)):
+        for gi, l in enumerate(grids):
+            X = rng.standard_normal(o.shape(l))
+            Xt = torch.from_numpy(X.ravel()).cuda()
+            Yt = torch.zeros_like(Xt)
+            g.sg_apply_strip_operator(set_, gi, Xt, Yt)
+            Y = Yt.cpu().numpy().reshape(X.shape)
+            ref = o.apply_diag(l, X)
+            assert relmax(Y, ref) <= 1e-12, (set_, l)
+
+
+@pytest.mark.parametrize("name", CONFIG_ORDER)
+def test_apply_full_cross_grid(name):
+    g, o = pair(name)
+    rng = np.random.default_rng(1)
+    U = {l: rng.standard_normal(o.shape(l)) for l in o.active}
+    Xt = from_blocks(g, U)
+    Yt = torch.zeros_like(Xt)
+    g.sg_apply_full(Xt, Yt)
+    Y = to_blocks(g, Yt)
+    ref = o.apply_full(o.terms, U)
+    for l in o.active:
+        assert relmax(Y[l], ref[l]) <= 1e-12, l
+
+
+@pytest.mark.parametrize("name", ["c1_2d_rot", "c3_4d_lshape", "c4_6d_stream"])
+def test_apply_mass_full(name):
+    from oracle.problem import mass_terms
+    g, o = pair(name)
+    rng = np.random.default_rng(2)
+    Tb = rng.standard_normal((o.S, 1))
+    U = {l: rng.standard_normal((1,) + o.shape(l)[1:]) for l in o.active}
+    Xt = from_blocks(g, U, S=1)
+    Yt = torch.zeros(g.set_size(SET_ACTIVE, o.S), dtype=torch.float64, device="cuda")
+    g.sg_apply_mass_full(Tb, Xt, Yt)
+    Y = to_blocks(g, Yt)
+    ref = o.apply_full(mass_terms(o.cfg, Tb), U)
+    for l in o.active:
+        assert relmax(Y[l], ref[l]) <= 1e-12, l
+
+
+@pytest.mark.parametrize("name", ["c0_2d_const", "c3_4d_lshape", "c4_6d_stream"])
+def test_transfers_and_combine(name):
+    g, o = pair(name)
+    rng = np.random.default_rng(3)
+    S = o.S
+    for fac, which in ((0, "x"), (1, "v")):
+        for lf in range(2, o.F + 1):
+            lo_ = 1
+            n_o = (o.Hv if fac == 0 else o.Hx).n(lo_)
+            nc, nf = (o.Hx if fac == 0 else o.Hv).n(lf - 1), (o.Hx if fac == 0 else o.Hv).n(lf)
+            shp_c = (S, nc, n_o) if fac == 0 else (S, n_o, nc)
+            shp_f = (S, nf, n_o) if fac == 0 else (S, n_o, nf)
+            u = rng.standard_normal(shp_c)
+            out = torch.zeros(int(np.prod(shp_f)), dtype=torch.float64, device="cuda")
+            g.sg_prolongate(fac, lf, lf - 1, lo_, S, torch.from_numpy(u.ravel()).cuda(), out)
+            ref = o.prolong(which, u, lf, lf - 1)
+            assert np.array_equal(out.cpu().numpy().reshape(shp_f), ref)       # exact: weights 1, 1/2
+            r = rng.standard_normal(shp_f)
+            out2 = torch.zeros(int(np.prod(shp_c)), dtype=torch.float64, device="cuda")
+            g.sg_restrict(fac, lf - 1, lf, lo_, S, torch.from_numpy(r.ravel()).cuda(), out2)
+            assert relmax(out2.cpu().numpy().reshape(shp_c), o.restrict(which, r, lf - 1, lf)) <= 1e-15
+    dh = {l: rng.standard_normal(o.shape(l)) for l in o.active + o.coarse}
+    du = torch.zeros(g.set_size(SET_ACTIVE, S), dtype=torch.float64, device="cuda")
+    g.sg_combine(from_blocks(g, dh), from_blocks(g, dh, SET_COARSE), du)
+    ref = o.combine(dh)
+    got = to_blocks(g, du)
+    for l in o.active:
+        assert relmax(got[l], ref[l]) <= 1e-15
+
+
+@pytest.mark.parametrize("name", CONFIG_ORDER)
+def test_interp_u0_and_rhs(name):
+    g, o = pair(name)
+    u0 = torch.zeros(g.set_size(SET_ACTIVE, 1), dtype=torch.float64, device="cuda")
+    g.sg_interp_u0(u0)
+    ref = o.interp_u0()
+    got = to_blocks(g, u0, S=1)
+    for l in o.active:
+        assert relmax(got[l], ref[l]) <= 1e-14, l
+    for j in (1, 3):
+        b = torch.zeros(g.set_size(SET_ACTIVE, o.S), dtype=torch.float64, device="cuda")
+        g.sg_rhs(j, u0, b)
+        rb = o.rhs(j, ref)
+        gb = to_blocks(g, b)
+        for l in o.active:
+            assert relmax(gb[l], rb[l]) <= 1e-12, (j, l)
+
+
+def _full(o, blocks):
+    return o.to_full(blocks)
+
+
+@pytest.mark.parametrize("name", CONFIG_ORDER)
+def test_solve_strip(name):
+    """Richardson + combination preconditioner: same FUNCTION as the oracle (coefficients
+    are a spanning-set representation, not unique)."""
+    g, o = pair(name)
+    tr0 = o.interp_u0()
+    b = o.rhs(1, tr0)
+    U, it, _ = o.solve_strip(b, rtol=1e-13)
+    bt = from_blocks(g, b)
+    ut = torch.zeros_like(bt)
+    git, last = g.sg_solve_strip(bt, ut, rtol=1e-13, inner_rtol=1e-13, max_iter=200)
+    G = to_blocks(g, ut)
+    for s in range(o.S):
+        f_ref = _full(o, {l: U[l][s:s + 1] for l in o.active})
+        f_gpu = _full(o, {l: G[l][s:s + 1] for l in o.active})
+        assert relmax(f_gpu, f_ref) <= 1e-9, (s, it, git)
+
+
+@pytest.mark.parametrize("name", CONFIG_ORDER)
+def test_step_matches_oracle(name):
+    g, o = pair(name)
+    nst = 3
+    tr_ref, _, _ = o.run(nsteps=nst, rtol=1e-13)
+    u0 = torch.zeros(g.set_size(SET_ACTIVE, 1), dtype=torch.float64, device="cuda")
+    g.sg_interp_u0(u0)
+    g.sg_step(1, nst, u0, rtol=1e-13, inner_rtol=1e-13)
+    f_ref = _full(o, tr_ref)
+    f_gpu = _full(o, to_blocks(g, u0, S=1))
+    assert relmax(f_gpu, f_ref) <= 1e-9
+    # host-buffer path (e2e) gives the same result
+    h = np.zeros(g.set_size(SET_ACTIVE, 1))
+    g.sg_interp_u0(u0)
+    h[:] = u0.cpu().numpy()
+    g.sg_step(1, nst, h, rtol=1e-13, inner_rtol=1e-13)
+    f_h = _full(o, to_blocks(g, torch.from_numpy(h), S=1))
+    assert relmax(f_h, f_ref) <= 1e-9
+
+
+def test_single_grid_edge_case():
+    """L = 2: one component grid, no coarse grids; the preconditioner is exact."""
+    g, o = pair("c1_2d_rot", L=2)
+    assert g.num_grids(SET_COARSE) == 0
+    tr0 = o.interp_u0()
+    b = o.rhs(1, tr0)
+    U, it, _ = o.solve_strip(b, rtol=1e-13)
+    ut = torch.zeros(g.set_size(SET_ACTIVE, o.S), dtype=torch.float64, device="cuda")
+    git, _ = g.sg_solve_strip(from_blocks(g, b), ut, rtol=1e-13, inner_rtol=1e-13)
+    assert git <= 3
+    G = to_blocks(g, ut)
+    for l in o.active:
+        assert relmax(G[l], U[l]) <= 1e-10
+
+
+def test_zero_rhs_gives_zero():
+    g, o = pair("c2_4d_stream")
+    b = torch.zeros(g.set_size(SET_ACTIVE, o.S), dtype=torch.float64, device="cuda")
+    u = torch.zeros_like(b)
+    it, last = g.sg_solve_strip(b, u)
+    assert it == 1 and float(u.abs().max()) == 0.0
