@@ -1,0 +1,264 @@
+#!/usr/bin/env python
+"""Benchmark of the sparse-grid dG streamline-diffusion strip solver on B200.
+
+A "step" is one time strip of the paper's method (eq. (4)): the jump
+and inflow load, the Richardson iteration with the combination-technique
+preconditioner (l.540-566) whose block solves apply the per-grid strip
+operator sum_t T_t (x) A_t (x) B_t (the hot path), the cross-grid residual,
+and the trace.  Metric: strip-operator DOF-applies/s (whole job), plus time
+steps/s and the roofline of the strip-operator kernels.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl reference]
+
+N > 1 runs N independent replicas ("replicas only": the method does not
+shard), one per rank under torchrun; value = sum over ranks.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DEFAULT_CONFIG = "c4_6d_stream"
+METRIC = "strip-operator DOF-applies/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=DEFAULT_CONFIG)
+    ap.add_argument("--L", type=int, default=None, help="override combination level (not a bench line)")
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--rtol", type=float, default=1e-10)
+    ap.add_argument("--inner-rtol", type=float, default=1e-10)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.check_output(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                               "--format=csv,noheader,nounits"], timeout=5).decode().strip()
+                self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = sorted(float(s[0]) for s in self.samples)
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            for n, v in zip(names, s[3:7]):
+                if "Active" in v and "Not" not in v:
+                    reasons.add(n)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(self.samples[0][1]), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def cpu_baseline(cfg_name, budget_s=15.0):
+    """The oracle (unmodified) timed on the host cores on a bounded sample of the
+    same workload: strip-operator applies on the component grids of the same
+    configuration family at a reduced combination level (sample stated)."""
+    import numpy as np
+    from oracle.sgrid import SGProblem
+    from sginputs import get_config
+    L0 = {"c0_2d_const": 6, "c1_2d_rot": 10, "c2_4d_stream": 7, "c3_4d_lshape": 6, "c4_6d_stream": 5}[cfg_name]
+    cfg = get_config(cfg_name, L=L0)
+    o = SGProblem(cfg, galerkin="direct")
+    rng = np.random.default_rng(0)
+    X = {l: rng.standard_normal(o.shape(l)) for l in o.active}
+    for l in o.active:        # assembly outside the timed region
+        o.apply_diag(l, X[l])
+    dof = 0
+    t0 = time.perf_counter()
+    n = 0
+    while time.perf_counter() - t0 < budget_s or n == 0:
+        for l in o.active:
+            o.apply_diag(l, X[l])
+            dof += int(np.prod(o.shape(l)))
+        n += 1
+    dt = time.perf_counter() - t0
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count()
+    return {"value": dof / dt, "unit": "DOF-applies/s", "cores": cores, "kind": "oracle",
+            "sample": f"oracle apply_diag over all {len(o.active)} active grids of {cfg_name} at L={L0} "
+                      f"({sum(int(np.prod(o.shape(l))) for l in o.active)} DOF/sweep), {n} sweeps, {dt:.1f}s",
+            "threads_note": "numpy/scipy default threading"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cb = cpu_baseline(args.config, budget_s=max(5.0, 20.0 / max(args.steps, 1)))
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "DOF-applies/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "dtype": "f64", "data": "synthetic", "vs_baseline": None,
+            "config": {"workload": args.config, "note": "oracle on host cores, bounded sample"},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "DOF-applies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    import torch
+    import torch.distributed as dist
+    from paper_2204_05988_b200 import Problem
+    from sginputs import get_config
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg_over = {} if args.L is None else {"L": args.L}
+    cfg = get_config(args.config, **cfg_over)
+    stream = torch.cuda.current_stream()
+    t_setup = time.perf_counter()
+    prob = Problem(cfg, stream=stream)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
+    N = int(round(cfg["T"] / cfg["tau"]))
+    n_tr = prob.set_size(0, 1)
+    trace = torch.zeros(n_tr, dtype=torch.float64, device="cuda")
+    prob.sg_interp_u0(trace)
+    j = 1
+    # warmup strips
+    for _ in range(args.warmup):
+        prob.sg_step(j, 1, trace, args.rtol, args.inner_rtol)
+        j += 1
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    prob.reset_stats()
+    prob.set_timing(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            prob.sg_step(j, 1, trace, args.rtol, args.inner_rtol)
+            j += 1
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    st = prob.stats()
+    kt = prob.kernel_time()
+    prob.set_timing(False)
+    if world > 1:
+        t = torch.tensor([ms, float(st["dof_applied"])], dtype=torch.float64, device="cuda")
+        mx = t.clone(); dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t.clone(); dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_max, dof_all = float(mx[0]), float(sm[1])
+    else:
+        ms_max, dof_all = ms, float(st["dof_applied"])
+    value = dof_all / (ms_max / 1e3)
+    # ------------------------------------------------------------- e2e (host buffers)
+    e2e = None
+    if not args.no_e2e:
+        import numpy as np
+        host = torch.empty(n_tr, dtype=torch.float64).pin_memory()
+        host.copy_(trace)
+        hnp = host.numpy()
+        prob.reset_stats()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        je = j - args.steps
+        for _ in range(args.steps):
+            prob.sg_step(je, 1, hnp, args.rtol, args.inner_rtol)   # H2D trace, strip, D2H trace
+            je += 1
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t[0])
+        st2 = prob.stats()
+        dof2 = float(st2["dof_applied"]) * world
+        e2e = {"value": dof2 / dt, "unit": "DOF-applies/s", "h2d_bytes_per_step": 8 * n_tr,
+               "d2h_bytes_per_step": 8 * n_tr, "time_steps_per_s": args.steps * world / dt}
+    # ---------------------------------------------------------------- roofline
+    pk = peaks()
+    hbm = pk.get("hbm_gbs", 6650.0)
+    per_launch_ms = kt["ms"] / max(kt["launches"], 1)
+    achieved = (kt["bytes"] / 1e9) / (kt["ms"] / 1e3) if kt["ms"] > 0 else None
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": (achieved / hbm) if achieved else None, "traffic": None,
+            "kernel": "strip-operator apply (k_fanout<1,W,*> + k_gather<0,W>) per component grid",
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback 6650 GB/s",
+            "flops_achieved_gflops": (kt["flops"] / 1e9) / (kt["ms"] / 1e3) if kt["ms"] > 0 else None,
+            "share_of_step": (kt["ms"] / ms) if ms > 0 else None,
+            "avg_apply_ms": kt["ms"] / max(st["applies"], 1)}
+    clocks = clk.summary()
+    out = {"metric": METRIC, "value": value, "unit": "DOF-applies/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": cfg["name"], "L": cfg["L"], "d": cfg["d"], "q": cfg["q"], "tau": cfg["tau"],
+                      "strips_total": N, "parallelism": f"replicas{world}",
+                      "l2": "inputs larger than L2 (component grids up to %.0f MB)" % (
+                          max(prob.grid_info(0, g)[2] * prob.grid_info(0, g)[3] for g in range(prob.num_grids(0)))
+                          * 8 * prob.S / 1e6),
+                      "rtol": args.rtol, "inner_rtol": args.inner_rtol,
+                      "dof_active": prob.set_size(0, prob.S)},
+           "time_steps_per_s": args.steps * world / (ms_max / 1e3),
+           "gpu_launches": st["launches"],
+           "applies": st["applies"], "outer_iters": st["outer_iters"], "inner_iters": st["inner_iters"],
+           "setup_s": t_setup, "roofline": roof, "clocks": clocks, "e2e": e2e}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            out["cpu_baseline"] = cpu_baseline(cfg["name"])
+        except Exception as ex:  # never fail the bench line on the baseline leg
+            out["cpu_baseline"] = {"error": str(ex)}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -140,6 +140,7 @@ extern "C" int sg_assemble_factors(sg_problem* P) {
     }
     for (auto& g : P->vgroups) SG_TRY(combine_group(P, g, true));
     for (auto& g : P->xgroups) SG_TRY(combine_group(P, g, false));
+    SG_TRY(prepare_stencils(P));
     // workspaces
     int64_t maxg = 0;
     for (auto& g : P->active) maxg = std::max(maxg, g.n1 * g.n2);
@@ -154,6 +155,7 @@ extern "C" int sg_assemble_factors(sg_problem* P) {
     P->wsZ_n = (size_t)std::max<int64_t>(std::max<int64_t>(nbz * S * maxg, S * chain), S * chain_up);
     P->wsA_n = P->wsB_n = (size_t)(S * maxg);
     SG_CUDA(cudaMalloc(&P->wsZ, sizeof(double) * P->wsZ_n));
+    SG_CUDA(cudaMemsetAsync(P->wsZ, 0, sizeof(double) * P->wsZ_n, P->stream));   // finite garbage only
     SG_CUDA(cudaMalloc(&P->wsA, sizeof(double) * P->wsA_n));
     SG_CUDA(cudaMalloc(&P->wsB, sizeof(double) * P->wsB_n));
     const int64_t Na = set_size(P, SG_SET_ACTIVE, S), Nc = set_size(P, SG_SET_COARSE, S);
@@ -163,10 +165,12 @@ extern "C" int sg_assemble_factors(sg_problem* P) {
     SG_CUDA(cudaMemset(P->scal, 0, sizeof(double) * 10 * (MAX_SEG + 1)));
     SG_CUDA(cudaMallocHost(&P->hscal, sizeof(double) * 10 * (MAX_SEG + 1)));
     const int64_t nF = std::max(P->fx.lev[F].n, P->fv.lev[F].n) + 16;
-    const int64_t sizes[13] = {Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na, Na + Nc, Na + Nc, Na,
-                               std::max(Na, 4 * nF), Na, Na};
-    P->vec.assign(13, nullptr);
-    for (int i = 0; i < 13; ++i) SG_CUDA(cudaMalloc(&P->vec[i], sizeof(double) * sizes[i]));
+    const int64_t sizes[15] = {Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na, Na + Nc, Na + Nc, Na,
+                               std::max(Na, 4 * nF), Na, Na, Na + Nc, Na + Nc};
+    P->vec.assign(15, nullptr);
+    for (int i = 0; i < 15; ++i) SG_CUDA(cudaMalloc(&P->vec[i], sizeof(double) * sizes[i]));
+    P->use_precond = getenv("SG_NO_PRECOND") == nullptr;
+    SG_TRY(build_block_jacobi(P));
     SG_CUDA(cudaMalloc(&P->trace_dev, sizeof(double) * set_size(P, SG_SET_ACTIVE, 1)));
     SG_CUDA(cudaStreamSynchronize(P->stream));
     P->assembled = true;
@@ -175,7 +179,9 @@ extern "C" int sg_assemble_factors(sg_problem* P) {
 
 static void free_level(Level& L) {
     cudaFree(L.lat); cudaFree(L.cols); cudaFree(L.pcols); cudaFree(L.pvals); cudaFree(L.rcols); cudaFree(L.rvals);
+    cudaFree(L.bflag);
     for (double* p : L.fm) cudaFree(p);
+    for (double* p : L.fst) cudaFree(p);
 }
 
 extern "C" void sg_destroy(sg_problem* P) {
@@ -186,11 +192,15 @@ extern "C" void sg_destroy(sg_problem* P) {
     for (auto* gs : {&P->vgroups, &P->xgroups})
         for (auto& g : *gs)
             for (auto& lv : g.comb)
-                for (auto& ce : lv) cudaFree(ce.vals);
+                for (auto& ce : lv) {
+                    cudaFree(ce.vals);
+                    cudaFree(ce.st);
+                }
     cudaFree(P->wsZ); cudaFree(P->wsA); cudaFree(P->wsB); cudaFree(P->red); cudaFree(P->scal);
     if (P->hscal) cudaFreeHost(P->hscal);
     for (double* v : P->vec) cudaFree(v);
     cudaFree(P->trace_dev);
+    cudaFree(P->dinv);
     for (auto& pr : P->ev_pairs) {
         cudaEventDestroy(pr.first);
         cudaEventDestroy(pr.second);

@@ -11,6 +11,8 @@
 // Matrices are column-major ELL: vals[k * nrows + row], cols[k * nrows + row]
 // (-1 padded, value 0).  Threads are flattened over (r, c) with c fastest so
 // every warp reads consecutive c (coalesced rows of the block).
+#include <algorithm>
+
 #include "sg_internal.cuh"
 
 namespace sg {
@@ -190,6 +192,242 @@ int launch_copy(sg_problem* P, int64_t n, const double* x, double* y) {
 int launch_zero(sg_problem* P, int64_t n, double* y) {
     if (n == 0) return SG_OK;
     SG_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * n, P->stream));
+    return SG_OK;
+}
+
+
+
+// =====================================================================
+// Stencil-format kernels for box-lattice factors (v2 hot path).
+//
+// On a box lattice numbered lexicographically, the Kuhn P1 neighbours of
+// node i are i + off_k with 2^(d+1)-1 constant offsets (d = 1: 3, d = 2: 7,
+// d = 3: 15); sorted ascending they form runs of consecutive integers
+// ("bands": d = 1: {3}; d = 2: {2,3,2}; d = 3: {2,2,2,3,2,2,2}).  A factor
+// matrix is stored as st[k][i] = A[i, i + off_k] (0 where the neighbour is
+// absent).  Sharing the band loads between T consecutive target rows cuts the
+// loads per output from W to about (W + 2 * bands * ...) / T.
+// =====================================================================
+namespace stc {
+template <int D> struct Bands;
+template <> struct Bands<1> {
+    static constexpr int NB = 1, W = 3;
+    __host__ __device__ static constexpr int lo(int) { return 0; }
+    __host__ __device__ static constexpr int len(int) { return 3; }
+};
+template <> struct Bands<2> {
+    static constexpr int NB = 3, W = 7;
+    __host__ __device__ static constexpr int lo(int b) { return b == 0 ? 0 : (b == 1 ? 2 : 5); }
+    __host__ __device__ static constexpr int len(int b) { return b == 1 ? 3 : 2; }
+};
+template <> struct Bands<3> {
+    static constexpr int NB = 7, W = 15;
+    __host__ __device__ static constexpr int lo(int b) { return b < 3 ? 2 * b : (b == 3 ? 6 : 9 + 2 * (b - 4)); }
+    __host__ __device__ static constexpr int len(int b) { return b == 3 ? 3 : 2; }
+};
+}  // namespace stc
+
+__global__ void k_ell_to_stencil(int64_t n, int W, const int32_t* __restrict__ cols, const double* __restrict__ vals,
+                                 StencilOff so, double* __restrict__ out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double v[15];
+    for (int k = 0; k < W; ++k) v[k] = 0.0;
+    for (int e = 0; e < W; ++e) {
+        int32_t c = cols[e * n + i];
+        if (c < 0) continue;
+        int64_t off = (int64_t)c - i;
+        for (int k = 0; k < W; ++k)
+            if (so.off[k] == off) v[k] += vals[e * n + i];
+    }
+    for (int k = 0; k < W; ++k) out[k * n + i] = v[k];
+}
+
+int launch_ell_to_stencil(sg_problem* P, int64_t n, int W, const int32_t* cols, const double* vals,
+                          const StencilOff& so, double* out) {
+    k_ell_to_stencil<<<(int)((n + 255) / 256), 256, 0, P->stream>>>(n, W, cols, vals, so, out);
+    P->launches++;
+    SG_CUDA(cudaGetLastError());
+    return SG_OK;
+}
+
+// Pass 1 (v side): Z_g[row][a] = sum_k Bst_g[k][a] X[row][a + off_k] for all groups g,
+// row = (s, j) over S*n1 rows.  Block = 64 columns x 4 row lanes; the block's
+// coefficients live in shared memory [g][k][64] and are reused for all rows
+// of the block; each thread handles R rows at a time (registers).  Groups with
+// index >= ng_int are only needed on x-boundary rows (face terms).
+template <int D, int R>
+__global__ void __launch_bounds__(256) k_vfan_st(int64_t nrows, int64_t n1, int64_t n2, StencilOff so,
+                                                 const uint8_t* __restrict__ xflag, VfanParams vp,
+                                                 const double* __restrict__ X, int64_t rows_per_block) {
+    constexpr int W = stc::Bands<D>::W;
+    extern __shared__ double sm[];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int64_t a = blockIdx.x * 64 + tx;
+    const bool aval = a < n2;
+    const int tot = vp.ng * W * 64;
+    for (int idx = ty * 64 + tx; idx < tot; idx += 256) {
+        const int g = idx / (W * 64), rem = idx - g * W * 64, k = rem >> 6, c = rem & 63;
+        const int64_t ac = blockIdx.x * 64 + c;
+        sm[idx] = ac < n2 ? __ldg(vp.vst[g] + k * n2 + ac) : 0.0;
+    }
+    __syncthreads();
+    int64_t addr[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        int64_t c = a + so.off[k];
+        addr[k] = c < 0 ? 0 : (c >= n2 ? n2 - 1 : c);
+    }
+    const int64_t rb = blockIdx.y * rows_per_block;
+    const int64_t re = min(nrows, rb + rows_per_block);
+    for (int64_t r0 = rb + ty * R; r0 < re; r0 += 4 * R) {
+        double x[R][W];
+        bool anyb = false;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int64_t row = r0 + r;
+            const bool ok = row < re && aval;
+            const double* base = X + (ok ? row : 0) * n2;
+#pragma unroll
+            for (int k = 0; k < W; ++k) x[r][k] = ok ? __ldg(base + addr[k]) : 0.0;
+            if (row < re) anyb |= xflag[row % n1] != 0;
+        }
+        const int ngu = anyb ? vp.ng : vp.ng_int;
+        for (int g = 0; g < ngu; ++g) {
+            double acc[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[r] = 0.0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                const double c = sm[(g * W + k) * 64 + tx];
+#pragma unroll
+                for (int r = 0; r < R; ++r) acc[r] = fma(c, x[r][k], acc[r]);
+            }
+            double* o = vp.out[g];
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (r0 + r < re && aval) o[(r0 + r) * n2 + a] = acc[r];
+        }
+    }
+}
+
+// Pass 2 (x side): Y[s][i][a] = beta*Y + sum_e [s_out(e)=s] sum_k Cst_e[k][i] Z_e[s_in][i + off_k][a].
+// Warp = 32 columns of T consecutive target rows i0..i0+T-1; 8 warps per block.
+template <int D, int T, int SO>
+__global__ void __launch_bounds__(256) k_xgat_st(int64_t n1, int64_t n2, StencilOff so,
+                                                 const uint8_t* __restrict__ xflag, XgatParams ep,
+                                                 double* __restrict__ Y, double beta, int64_t ncoltiles) {
+    using B = stc::Bands<D>;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t blk = blockIdx.x;
+    const int64_t ct = blk % ncoltiles, rg = blk / ncoltiles;
+    const int64_t i0 = (rg * 8 + warp) * T;
+    if (i0 >= n1) return;
+    const int64_t a = ct * 32 + lane;
+    const bool aval = a < n2;
+    const int64_t ac = aval ? a : 0;
+    bool anyb = false;
+#pragma unroll
+    for (int t = 0; t < T; ++t)
+        if (i0 + t < n1) anyb |= xflag[i0 + t] != 0;
+    double acc[SO][T];
+#pragma unroll
+    for (int s = 0; s < SO; ++s)
+#pragma unroll
+        for (int t = 0; t < T; ++t) acc[s][t] = 0.0;
+    const int64_t plane = n1 * n2;
+    for (int e = 0; e < ep.ne; ++e) {
+        if (ep.e[e].bonly && !anyb) continue;
+        const double* Z = ep.e[e].in + (int64_t)ep.e[e].s_in * plane;
+        const double* C = ep.e[e].cst;
+        const int so_ = ep.e[e].s_out;
+        double tmp[T];
+#pragma unroll
+        for (int t = 0; t < T; ++t) tmp[t] = 0.0;
+#pragma unroll
+        for (int b = 0; b < B::NB; ++b) {
+            constexpr int MAXL = 3;
+            const int klo = B::lo(b), len = B::len(b);
+            const int64_t base = i0 + so.off[klo];
+            double z[T + MAXL - 1];
+#pragma unroll
+            for (int q = 0; q < T + MAXL - 1; ++q) {
+                if (q < T + len - 1) {
+                    int64_t r = base + q;
+                    r = r < 0 ? 0 : (r >= n1 ? n1 - 1 : r);
+                    z[q] = __ldg(Z + r * n2 + ac);
+                }
+            }
+#pragma unroll
+            for (int kk = 0; kk < MAXL; ++kk) {
+                if (kk < len) {
+#pragma unroll
+                    for (int t = 0; t < T; ++t) {
+                        const int64_t it = i0 + t < n1 ? i0 + t : n1 - 1;
+                        tmp[t] = fma(__ldg(C + (int64_t)(klo + kk) * n1 + it), z[t + kk], tmp[t]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < SO; ++s)
+            if (s == so_)
+#pragma unroll
+                for (int t = 0; t < T; ++t) acc[s][t] += tmp[t];
+    }
+    if (!aval) return;
+#pragma unroll
+    for (int s = 0; s < SO; ++s)
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+            if (i0 + t >= n1) continue;
+            double* y = Y + (int64_t)s * plane + (i0 + t) * n2 + a;
+            *y = beta == 0.0 ? acc[s][t] : fma(beta, *y, acc[s][t]);
+        }
+}
+
+int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, const uint8_t* xflag,
+                   const VfanParams& vp, const double* X) {
+    const int W = (1 << (d + 1)) - 1;
+    const int64_t nrows = (int64_t)S * n1;
+    const int64_t ctiles = (n2 + 63) / 64;
+    // enough blocks to fill the machine, as many rows per block as possible (coefficient reuse)
+    int64_t rchunks = std::max<int64_t>(1, (148 * 4 + ctiles - 1) / ctiles);
+    rchunks = std::min<int64_t>(rchunks, (nrows + 7) / 8);
+    rchunks = std::max<int64_t>(rchunks, 1);
+    const int64_t rpb = (nrows + rchunks - 1) / rchunks;
+    const size_t smem = sizeof(double) * vp.ng * W * 64;
+    dim3 grid((unsigned)ctiles, (unsigned)rchunks), block(64, 4);
+    if (d == 1) {
+        cudaFuncSetAttribute(k_vfan_st<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_vfan_st<1, 4><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb);
+    } else if (d == 2) {
+        cudaFuncSetAttribute(k_vfan_st<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_vfan_st<2, 4><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb);
+    } else {
+        cudaFuncSetAttribute(k_vfan_st<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_vfan_st<3, 4><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb);
+    }
+    P->launches++;
+    SG_CUDA(cudaGetLastError());
+    return SG_OK;
+}
+
+int launch_xgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
+                   const uint8_t* xflag, const XgatParams& ep, double* Y, double beta) {
+    constexpr int T = 4;
+    const int64_t ctiles = (n2 + 31) / 32;
+    const int64_t rgroups = ((n1 + T - 1) / T + 7) / 8;
+    const int64_t nb = ctiles * rgroups;
+#define XG(DD, SS) k_xgat_st<DD, T, SS><<<(unsigned)nb, 256, 0, P->stream>>>(n1, n2, so, xflag, ep, Y, beta, ctiles)
+    if (S_out == 1) {
+        if (d == 1) XG(1, 1); else if (d == 2) XG(2, 1); else XG(3, 1);
+    } else {
+        if (d == 1) XG(1, 2); else if (d == 2) XG(2, 2); else XG(3, 2);
+    }
+#undef XG
+    P->launches++;
+    SG_CUDA(cudaGetLastError());
     return SG_OK;
 }
 

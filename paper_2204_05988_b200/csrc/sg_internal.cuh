@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -42,9 +43,15 @@ struct Spec {
     bool same(const Spec& o) const;
 };
 
+
 struct Term {
     double T[MAXS * MAXS];  // row-major S x S (row = test s, col = trial s')
     int xs, vs;             // spec ids in the x / v factor
+};
+
+// stencil offsets of a box-lattice level (sorted ascending; slot k <-> offset)
+struct StencilOff {
+    int64_t off[15];
 };
 
 // one level of one factor mesh
@@ -58,6 +65,9 @@ struct Level {
     int32_t* rcols = nullptr;   // restriction to level-1: [W][n_{l-1}]
     double* rvals = nullptr;
     std::vector<double*> fm;    // per spec id: [W][n], nullptr if unused
+    std::vector<double*> fst;   // per spec id: stencil format [W][n] (box lattices), nullptr if unused
+    uint8_t* bflag = nullptr;   // 1 for lattice-boundary nodes
+    StencilOff so;              // stencil offsets (box lattices)
 };
 
 struct Factor {
@@ -92,12 +102,30 @@ struct FanoutList {
 struct CombEntry {
     int s_out, s_in;
     double* vals;   // [W][n] device (owned)
+    double* st = nullptr;   // stencil format (box lattice of the other factor), owned
 };
 struct Group {                 // terms sharing one spec on the "inner" factor
     int spec;                  // shared spec id (v-spec for lower/x-groups, x-spec for upper)
     std::vector<int> terms;
+    bool bonly = false;        // other-factor matrices live on boundary rows only (face terms)
     // combined matrices of the OTHER factor per level: comb[level] = entries
     std::vector<std::vector<CombEntry>> comb;
+};
+
+constexpr int MAXG = 24;
+struct VfanParams {
+    int ng, ng_int;
+    const double* vst[MAXG];
+    double* out[MAXG];
+};
+struct XgatEntry {
+    const double* in;
+    const double* cst;
+    int s_out, s_in, bonly;
+};
+struct XgatParams {
+    int ne;
+    XgatEntry e[MAX_ENTRIES];
 };
 
 struct Grid {
@@ -125,6 +153,8 @@ struct sg_problem {
     std::vector<sg::Group> vgroups; // grouped by v-spec; comb = x-matrices (lower part / diag v-first)
     std::vector<sg::Group> xgroups; // grouped by x-spec; comb = v-matrices (upper part)
     int mass_x = -1, mass_v = -1;   // spec ids of the unweighted mass
+    std::vector<int> vorder;        // v-groups, interior first then boundary-only
+    int ng_int = 0;
     std::vector<sg::Grid> active, coarse;
     bool meshes_built = false, assembled = false;
     // workspaces
@@ -136,6 +166,8 @@ struct sg_problem {
     double* hscal = nullptr;                      // pinned host copy
     std::vector<double*> vec;                     // solver vectors
     double* trace_dev = nullptr;
+    double* dinv = nullptr;                       // block-Jacobi inverse (solve set)
+    bool use_precond = true;
     // instrumentation
     int64_t n_applies = 0, dof_applied = 0, launches = 0, outer_iters = 0, inner_iters = 0;
     bool timing = false;
@@ -158,9 +190,17 @@ int launch_gather(sg_problem* P, int dir, int W, int S_out, int64_t n1_in, int64
 int launch_axpby(sg_problem* P, int64_t n, double a, const double* x, double b, double* y);
 int launch_copy(sg_problem* P, int64_t n, const double* x, double* y);
 int launch_zero(sg_problem* P, int64_t n, double* y);
+int launch_ell_to_stencil(sg_problem* P, int64_t n, int W, const int32_t* cols, const double* vals,
+                          const StencilOff& so, double* out);
+int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, const uint8_t* xflag,
+                   const VfanParams& vp, const double* X);
+int launch_xgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
+                   const uint8_t* xflag, const XgatParams& ep, double* Y, double beta);
 // solver.cu
 int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y);
 int apply_cross(sg_problem* P, const std::vector<Term>* terms_override, const double* Tb, int S_out, int S_in,
                 const double* X, double* Y);
 int64_t set_size(const sg_problem* P, int set, int S);
+int build_block_jacobi(sg_problem* P);
+int prepare_stencils(sg_problem* P);
 }  // namespace sg

@@ -50,7 +50,7 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
     const int64_t n = gsize(g);
     const Level& Lx = P->fx.lev[g.l1];
     const Level& Lv = P->fv.lev[g.l2];
-    const int nb = (int)P->vgroups.size();
+    const int nb = (int)P->vorder.size();
     if ((size_t)nb * S * n > P->wsZ_n) {
         set_error("apply_diag: workspace too small");
         return SG_ERR_STATE;
@@ -58,31 +58,64 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
     cudaEvent_t e0 = nullptr;
     SG_TRY(timed_begin(P, &e0));
     int64_t l0 = P->launches;
-    for (int b0 = 0; b0 < nb; b0 += MAX_FANOUT) {
-        FanoutList fl;
-        fl.no = std::min(MAX_FANOUT, nb - b0);
-        for (int o = 0; o < fl.no; ++o) {
-            fl.vals[o] = Lv.fm[P->vgroups[b0 + o].spec];
-            fl.out[o] = P->wsZ + (int64_t)(b0 + o) * S * n;
+    const bool vbox = P->fv.kind == SG_MESH_BOX && nb <= MAXG;
+    const bool xbox = P->fx.kind == SG_MESH_BOX;
+    // ---- pass 1: Z_b = (Id x Id x B_b) X for every v-group b (interior groups first)
+    if (vbox) {
+        VfanParams vp;
+        vp.ng = nb;
+        vp.ng_int = P->ng_int;
+        for (int o = 0; o < nb; ++o) {
+            vp.vst[o] = Lv.fst[P->vgroups[P->vorder[o]].spec];
+            vp.out[o] = P->wsZ + (int64_t)o * S * n;
         }
-        SG_TRY(launch_fanout(P, 1, P->fv.W, S, g.n1, g.n2, g.n2, Lv.cols, X, fl));
-    }
-    EntryList el;
-    el.ne = 0;
-    double beta = 0.0;
-    int64_t nnz_x = 0;
-    for (int b = 0; b < nb; ++b) {
-        for (const auto& ce : P->vgroups[b].comb[g.l1]) {
-            if (el.ne == MAX_ENTRIES) {
-                SG_TRY(launch_gather(P, 0, P->fx.W, S, g.n1, g.n2, g.n1, Lx.cols, el, Y, beta));
-                beta = 1.0;
-                el.ne = 0;
+        SG_TRY(launch_vfan_st(P, P->fv.d, S, g.n1, g.n2, Lv.so, Lx.bflag, vp, X));
+    } else {
+        for (int b0 = 0; b0 < nb; b0 += MAX_FANOUT) {
+            FanoutList fl;
+            fl.no = std::min(MAX_FANOUT, nb - b0);
+            for (int o = 0; o < fl.no; ++o) {
+                fl.vals[o] = Lv.fm[P->vgroups[P->vorder[b0 + o]].spec];
+                fl.out[o] = P->wsZ + (int64_t)(b0 + o) * S * n;
             }
-            el.e[el.ne++] = {P->wsZ + (int64_t)b * S * n, ce.vals, 1.0, ce.s_out, ce.s_in};
-            nnz_x++;
+            SG_TRY(launch_fanout(P, 1, P->fv.W, S, g.n1, g.n2, g.n2, Lv.cols, X, fl));
         }
     }
-    SG_TRY(launch_gather(P, 0, P->fx.W, S, g.n1, g.n2, g.n1, Lx.cols, el, Y, beta));
+    // ---- pass 2: Y = sum_b sum_{s,s'} (e_s e_s'^T (x) C_b^{ss'} (x) Id) Z_b
+    int64_t nnz_x = 0;
+    double beta = 0.0;
+    if (xbox) {
+        XgatParams ep;
+        ep.ne = 0;
+        for (int o = 0; o < nb; ++o) {
+            const Group& gr = P->vgroups[P->vorder[o]];
+            for (const auto& ce : gr.comb[g.l1]) {
+                if (ep.ne == MAX_ENTRIES) {
+                    SG_TRY(launch_xgat_st(P, P->fx.d, S, g.n1, g.n2, Lx.so, Lx.bflag, ep, Y, beta));
+                    beta = 1.0;
+                    ep.ne = 0;
+                }
+                ep.e[ep.ne++] = {P->wsZ + (int64_t)o * S * n, ce.st, ce.s_out, ce.s_in, gr.bonly ? 1 : 0};
+                nnz_x++;
+            }
+        }
+        SG_TRY(launch_xgat_st(P, P->fx.d, S, g.n1, g.n2, Lx.so, Lx.bflag, ep, Y, beta));
+    } else {
+        EntryList el;
+        el.ne = 0;
+        for (int o = 0; o < nb; ++o) {
+            for (const auto& ce : P->vgroups[P->vorder[o]].comb[g.l1]) {
+                if (el.ne == MAX_ENTRIES) {
+                    SG_TRY(launch_gather(P, 0, P->fx.W, S, g.n1, g.n2, g.n1, Lx.cols, el, Y, beta));
+                    beta = 1.0;
+                    el.ne = 0;
+                }
+                el.e[el.ne++] = {P->wsZ + (int64_t)o * S * n, ce.vals, 1.0, ce.s_out, ce.s_in};
+                nnz_x++;
+            }
+        }
+        SG_TRY(launch_gather(P, 0, P->fx.W, S, g.n1, g.n2, g.n1, Lx.cols, el, Y, beta));
+    }
     P->n_applies++;
     P->dof_applied += S * n;
     // algorithmic bytes: read X, write Y, factor matrices (values + pattern)
@@ -90,6 +123,84 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
                    (8.0 * nnz_x + 4.0) * (double)(P->fx.W * g.n1);
     double flops = 2.0 * S * n * ((double)nb * P->fv.W + (double)nnz_x * P->fx.W);
     SG_TRY(timed_end(P, e0, bytes, flops, (int)(P->launches - l0)));
+    return SG_OK;
+}
+
+// stencil offsets / boundary flags / stencil-format matrices for box lattices
+__global__ void k_bflag(int64_t n, int d, int m, const int32_t* lat, uint8_t* f) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint8_t b = 0;
+    for (int k = 0; k < d; ++k) {
+        int z = lat[k * n + i];
+        b |= (z == 0 || z == m - 1);
+    }
+    f[i] = b;
+}
+
+int prepare_stencils(sg_problem* P) {
+    for (Factor* f : {&P->fx, &P->fv}) {
+        for (int l = 1; l <= P->F; ++l) {
+            Level& L = f->lev[l];
+            SG_CUDA(cudaMalloc(&L.bflag, L.n));
+            if (f->kind == SG_MESH_BOX) {
+                k_bflag<<<(int)((L.n + 255) / 256), 256, 0, P->stream>>>(L.n, f->d, L.m, L.lat, L.bflag);
+                P->launches++;
+                std::vector<int64_t> offs;
+                for (int S_ = 0; S_ < (1 << f->d); ++S_) {
+                    int64_t o = 0, st = 1;
+                    for (int i = 0; i < f->d; ++i) {
+                        if ((S_ >> i) & 1) o += st;
+                        st *= L.m;
+                    }
+                    offs.push_back(o);
+                    if (o) offs.push_back(-o);
+                }
+                std::sort(offs.begin(), offs.end());
+                for (int k = 0; k < 15; ++k) L.so.off[k] = k < (int)offs.size() ? offs[k] : 0;
+            } else {
+                SG_CUDA(cudaMemsetAsync(L.bflag, 1, L.n, P->stream));   // no skipping off box lattices
+            }
+        }
+    }
+    // group ordering: interior groups first, boundary-only (face) groups last
+    P->vorder.clear();
+    for (int pass = 0; pass < 2; ++pass)
+        for (size_t gi = 0; gi < P->vgroups.size(); ++gi) {
+            Group& g = P->vgroups[gi];
+            bool bonly = true;
+            for (int t : g.terms) bonly &= P->fx.specs[P->terms[t].xs].kind == 1;
+            g.bonly = bonly;
+            if ((pass == 0) != bonly) P->vorder.push_back((int)gi);
+        }
+    P->ng_int = 0;
+    for (int gi : P->vorder) P->ng_int += P->vgroups[gi].bonly ? 0 : 1;
+    for (auto& g : P->xgroups) {
+        bool bonly = true;
+        for (int t : g.terms) bonly &= P->fv.specs[P->terms[t].vs].kind == 1;
+        g.bonly = bonly;
+    }
+    // stencil-format copies
+    for (auto& g : P->vgroups) {
+        for (int l = 1; l <= P->F; ++l) {
+            if (P->fv.kind == SG_MESH_BOX) {
+                Level& L = P->fv.lev[l];
+                if ((int)L.fst.size() < (int)P->fv.specs.size()) L.fst.resize(P->fv.specs.size(), nullptr);
+                if (!L.fst[g.spec]) {
+                    SG_CUDA(cudaMalloc(&L.fst[g.spec], sizeof(double) * P->fv.W * L.n));
+                    SG_TRY(launch_ell_to_stencil(P, L.n, P->fv.W, L.cols, L.fm[g.spec], L.so, L.fst[g.spec]));
+                }
+            }
+            if (P->fx.kind == SG_MESH_BOX) {
+                Level& L = P->fx.lev[l];
+                for (auto& ce : g.comb[l]) {
+                    SG_CUDA(cudaMalloc(&ce.st, sizeof(double) * P->fx.W * L.n));
+                    SG_TRY(launch_ell_to_stencil(P, L.n, P->fx.W, L.cols, ce.vals, L.so, ce.st));
+                }
+            }
+        }
+    }
+    SG_CUDA(cudaStreamSynchronize(P->stream));
     return SG_OK;
 }
 
@@ -402,8 +513,8 @@ __global__ void k_bicg_s(SegTab t, const double* scal, const double* r, const do
 }
 
 // x += alpha p + omega s ; r = s - omega t ; partial dots (r0.r, r.r)
-__global__ void k_bicg_xr(SegTab tb, const double* scal, double* x, double* r, const double* p, const double* s,
-                          const double* t, const double* r0, double* partial) {
+__global__ void k_bicg_xr(SegTab tb, const double* scal, double* x, double* r, const double* p, const double* sx,
+                          const double* s, const double* t, const double* r0, double* partial) {
     __shared__ double sh[2][8];
     const int g = seg_of(tb, blockIdx.x);
     const double* sc = scal + g * NSC;
@@ -415,7 +526,7 @@ __global__ void k_bicg_xr(SegTab tb, const double* scal, double* x, double* r, c
     for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
         double ri = r[i];
         if (active) {
-            x[i] += al * p[i] + om * s[i];
+            x[i] += al * p[i] + om * sx[i];
             ri = s[i] - om * t[i];
             r[i] = ri;
         }
@@ -449,6 +560,114 @@ __global__ void k_bicg_p(SegTab t, const double* scal, double* p, const double* 
     for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) p[i] = r[i] + be * (p[i] - om * v[i]);
 }
 
+// ---------------------------------------------- point-block Jacobi (time)
+// D_k = sum_t T_t diag(A_t)_i diag(B_t)_a, an S x S block per node k = (i, a);
+// the inner solver is right-preconditioned with D^{-1} (the paper
+// uses GMRES+ILU for eq. (15); this is the GPU-friendly point-block variant).
+struct DiagTerm {
+    double T[4];
+    const double* dA;
+    const double* dB;
+};
+__global__ void k_extract_diag(int64_t n, int W, const int32_t* cols, const double* vals, double* out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double d = 0.0;
+    for (int k = 0; k < W; ++k)
+        if (cols[k * n + i] == (int32_t)i) d += vals[k * n + i];
+    out[i] = d;
+}
+__global__ void k_diag_block_inv(int64_t n1, int64_t n2, int S, int nt, const DiagTerm* terms, double* Dinv) {
+    const int64_t n = n1 * n2;
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int64_t i = k / n2, a = k - i * n2;
+    double D[4] = {0, 0, 0, 0};
+    for (int t = 0; t < nt; ++t) {
+        const double f = terms[t].dA[i] * terms[t].dB[a];
+        for (int q = 0; q < S * S; ++q) D[q] += terms[t].T[q] * f;
+    }
+    if (S == 1) {
+        Dinv[k] = 1.0 / D[0];
+    } else {
+        const double det = D[0] * D[3] - D[1] * D[2];
+        Dinv[0 * n + k] = D[3] / det;
+        Dinv[1 * n + k] = -D[1] / det;
+        Dinv[2 * n + k] = -D[2] / det;
+        Dinv[3 * n + k] = D[0] / det;
+    }
+}
+
+int build_block_jacobi(sg_problem* P) {
+    const int S = P->S;
+    std::vector<const Grid*> gr;
+    for (auto& g : P->active) gr.push_back(&g);
+    for (auto& g : P->coarse) gr.push_back(&g);
+    int64_t tot = 0;
+    for (auto* g : gr) tot += (int64_t)S * S * gsize(*g);
+    SG_CUDA(cudaMalloc(&P->dinv, sizeof(double) * tot));
+    // diagonal vectors of every used spec on every level
+    auto diagvec = [&](Factor& f, int spec, int l, double** out) -> int {
+        Level& L = f.lev[l];
+        SG_CUDA(cudaMalloc(out, sizeof(double) * L.n));
+        k_extract_diag<<<(int)((L.n + 255) / 256), 256, 0, P->stream>>>(L.n, f.W, L.cols, L.fm[spec], *out);
+        P->launches++;
+        return SG_OK;
+    };
+    std::vector<double*> tmp;
+    DiagTerm* dterms;
+    SG_CUDA(cudaMalloc(&dterms, sizeof(DiagTerm) * P->terms.size()));
+    int64_t off = 0;
+    for (auto* g : gr) {
+        std::vector<DiagTerm> ht;
+        for (auto& t : P->terms) {
+            DiagTerm d;
+            for (int q = 0; q < 4; ++q) d.T[q] = t.T[q];
+            double *a, *b;
+            SG_TRY(diagvec(P->fx, t.xs, g->l1, &a));
+            SG_TRY(diagvec(P->fv, t.vs, g->l2, &b));
+            tmp.push_back(a);
+            tmp.push_back(b);
+            d.dA = a;
+            d.dB = b;
+            ht.push_back(d);
+        }
+        SG_CUDA(cudaMemcpyAsync(dterms, ht.data(), sizeof(DiagTerm) * ht.size(), cudaMemcpyHostToDevice, P->stream));
+        const int64_t n = gsize(*g);
+        k_diag_block_inv<<<(int)((n + 255) / 256), 256, 0, P->stream>>>(g->n1, g->n2, S, (int)ht.size(), dterms,
+                                                                       P->dinv + off);
+        P->launches++;
+        SG_CUDA(cudaGetLastError());
+        SG_CUDA(cudaStreamSynchronize(P->stream));
+        for (double* q : tmp) cudaFree(q);
+        tmp.clear();
+        off += (int64_t)S * S * n;
+    }
+    cudaFree(dterms);
+    return SG_OK;
+}
+
+// out = D^{-1} in on every segment (segment = one grid, S x n block)
+__global__ void k_seg_precond(SegTab t, int S, const double* scal, const double* Dinv, const double* in, double* out) {
+    const int g = seg_of(t, blockIdx.x);
+    if (scal[g * NSC + 5] != 0.0) return;
+    const int64_t base = t.off[g];
+    const int64_t n = (t.off[g + 1] - base) / S;
+    const double* Dg = Dinv + base * S;
+    const int64_t lo = base + (int64_t)(blockIdx.x - t.blk[g]) * SEG_CHUNK;
+    const int64_t hi = min(lo + SEG_CHUNK, t.off[g + 1]);
+    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+        if (S == 1) {
+            out[e] = Dg[e - base] * in[e];
+        } else {
+            const int64_t le = e - base;
+            const int s = (int)(le / n);
+            const int64_t k = le - s * n;
+            out[e] = Dg[(s * 2 + 0) * n + k] * in[base + k] + Dg[(s * 2 + 1) * n + k] * in[base + n + k];
+        }
+    }
+}
+
 // batched BiCGStab on the grids `gr` (block solves of eq. (15)); b, x concatenated in order of gr
 static int bicgstab(sg_problem* P, const std::vector<const Grid*>& gr, const double* b, double* x, double rtol,
                     int maxit) {
@@ -459,6 +678,8 @@ static int bicgstab(sg_problem* P, const std::vector<const Grid*>& gr, const dou
     SegTab t = make_segs(offs);
     const int nblk = t.blk[t.nseg];
     double *r = P->vec[0], *r0 = P->vec[1], *p = P->vec[2], *v = P->vec[3], *s = P->vec[4], *tt = P->vec[5];
+    double *ph = P->vec[13], *sh = P->vec[14];
+    const bool pc = P->dinv != nullptr && P->use_precond;
     SG_TRY(launch_zero(P, N, x));
     SG_TRY(launch_copy(P, N, b, r));
     SG_TRY(launch_copy(P, N, b, r0));
@@ -469,17 +690,29 @@ static int bicgstab(sg_problem* P, const std::vector<const Grid*>& gr, const dou
     const double tol2 = rtol * rtol;
     std::vector<char> conv(gr.size(), 0);
     for (int it = 0; it < maxit; ++it) {
-        // v = A p
+        // v = A M^{-1} p
+        const double* pa = p;
+        if (pc) {
+            k_seg_precond<<<nblk, 256, 0, P->stream>>>(t, S, P->scal, P->dinv, p, ph);
+            P->launches++;
+            pa = ph;
+        }
         for (size_t i = 0; i < gr.size(); ++i)
-            if (!conv[i]) SG_TRY(apply_diag(P, *gr[i], p + offs[i], v + offs[i]));
+            if (!conv[i]) SG_TRY(apply_diag(P, *gr[i], pa + offs[i], v + offs[i]));
         k_seg_dot<1><<<nblk, 256, 0, P->stream>>>(t, r0, v, nullptr, nullptr, P->red);
         k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 1, P->red, P->scal, 6, 6, 1, tol2);
         k_bicg_s<<<nblk, 256, 0, P->stream>>>(t, P->scal, r, v, s);
+        const double* sa = s;
+        if (pc) {
+            k_seg_precond<<<nblk, 256, 0, P->stream>>>(t, S, P->scal, P->dinv, s, sh);
+            P->launches++;
+            sa = sh;
+        }
         for (size_t i = 0; i < gr.size(); ++i)
-            if (!conv[i]) SG_TRY(apply_diag(P, *gr[i], s + offs[i], tt + offs[i]));
+            if (!conv[i]) SG_TRY(apply_diag(P, *gr[i], sa + offs[i], tt + offs[i]));
         k_seg_dot<3><<<nblk, 256, 0, P->stream>>>(t, tt, s, tt, tt, P->red, s, s);
         k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 3, P->red, P->scal, 7, 8, 2, tol2);
-        k_bicg_xr<<<nblk, 256, 0, P->stream>>>(t, P->scal, x, r, p, s, tt, r0, P->red);
+        k_bicg_xr<<<nblk, 256, 0, P->stream>>>(t, P->scal, x, r, pa, sa, s, tt, r0, P->red);
         k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 2, P->red, P->scal, 0, 4, 3, tol2);
         k_bicg_p<<<nblk, 256, 0, P->stream>>>(t, P->scal, p, r, v);
         P->launches += 8;
