@@ -256,19 +256,21 @@ int launch_ell_to_stencil(sg_problem* P, int64_t n, int W, const int32_t* cols, 
 // coefficients live in shared memory [g][k][64] and are reused for all rows
 // of the block; each thread handles R rows at a time (registers).  Groups with
 // index >= ng_int are only needed on x-boundary rows (face terms).
+constexpr int VF_TC = 32;   // columns per block
+constexpr int VF_RL = 8;    // row lanes per block
 template <int D, int R>
-__global__ void __launch_bounds__(256) k_vfan_st(int64_t nrows, int64_t n1, int64_t n2, StencilOff so,
-                                                 const uint8_t* __restrict__ xflag, VfanParams vp,
-                                                 const double* __restrict__ X, int64_t rows_per_block) {
+__global__ void __launch_bounds__(VF_TC * VF_RL, 2) k_vfan_st(int64_t nrows, int64_t n1, int64_t n2, StencilOff so,
+                                                              const uint8_t* __restrict__ xflag, VfanParams vp,
+                                                              const double* __restrict__ X, int64_t rows_per_block) {
     constexpr int W = stc::Bands<D>::W;
     extern __shared__ double sm[];
     const int tx = threadIdx.x, ty = threadIdx.y;
-    const int64_t a = blockIdx.x * 64 + tx;
+    const int64_t a = blockIdx.x * VF_TC + tx;
     const bool aval = a < n2;
-    const int tot = vp.ng * W * 64;
-    for (int idx = ty * 64 + tx; idx < tot; idx += 256) {
-        const int g = idx / (W * 64), rem = idx - g * W * 64, k = rem >> 6, c = rem & 63;
-        const int64_t ac = blockIdx.x * 64 + c;
+    const int tot = vp.ng * W * VF_TC;
+    for (int idx = ty * VF_TC + tx; idx < tot; idx += VF_TC * VF_RL) {
+        const int g = idx / (W * VF_TC), rem = idx - g * W * VF_TC, k = rem / VF_TC, c = rem - k * VF_TC;
+        const int64_t ac = blockIdx.x * VF_TC + c;
         sm[idx] = ac < n2 ? __ldg(vp.vst[g] + k * n2 + ac) : 0.0;
     }
     __syncthreads();
@@ -280,7 +282,7 @@ __global__ void __launch_bounds__(256) k_vfan_st(int64_t nrows, int64_t n1, int6
     }
     const int64_t rb = blockIdx.y * rows_per_block;
     const int64_t re = min(nrows, rb + rows_per_block);
-    for (int64_t r0 = rb + ty * R; r0 < re; r0 += 4 * R) {
+    for (int64_t r0 = rb + ty * R; r0 < re; r0 += VF_RL * R) {
         double x[R][W];
         bool anyb = false;
 #pragma unroll
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(256) k_vfan_st(int64_t nrows, int64_t n1, int6
             for (int r = 0; r < R; ++r) acc[r] = 0.0;
 #pragma unroll
             for (int k = 0; k < W; ++k) {
-                const double c = sm[(g * W + k) * 64 + tx];
+                const double c = sm[(g * W + k) * VF_TC + tx];
 #pragma unroll
                 for (int r = 0; r < R; ++r) acc[r] = fma(c, x[r][k], acc[r]);
             }
@@ -312,77 +314,112 @@ __global__ void __launch_bounds__(256) k_vfan_st(int64_t nrows, int64_t n1, int6
 }
 
 // Pass 2 (x side): Y[s][i][a] = beta*Y + sum_e [s_out(e)=s] sum_k Cst_e[k][i] Z_e[s_in][i + off_k][a].
-// Warp = 32 columns of T consecutive target rows i0..i0+T-1; 8 warps per block.
-template <int D, int T, int SO>
-__global__ void __launch_bounds__(256) k_xgat_st(int64_t n1, int64_t n2, StencilOff so,
-                                                 const uint8_t* __restrict__ xflag, XgatParams ep,
-                                                 double* __restrict__ Y, double beta, int64_t ncoltiles) {
+// Block = 8 warps x T consecutive target rows (32 rows); warp lanes = columns,
+// CPT columns per lane.  The block's coefficients (chunk of entries) are staged
+// in shared memory and read as broadcasts; Z rows are shared between the T
+// targets of a warp band by band (Kuhn offsets form runs of consecutive rows).
+constexpr int XG_ECH = 12;   // entries per shared-memory chunk
+template <int D, int T, int SO, int CPT>
+__global__ void __launch_bounds__(256, 2) k_xgat_st(int n1, int n2, StencilOff so, const uint8_t* __restrict__ xflag,
+                                                    XgatParams ep, double* __restrict__ Y, double beta,
+                                                    int ncoltiles) {
     using B = stc::Bands<D>;
+    constexpr int W = B::W;
+    constexpr int ROWS = 8 * T;
+    __shared__ double cs[XG_ECH][W][ROWS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t blk = blockIdx.x;
-    const int64_t ct = blk % ncoltiles, rg = blk / ncoltiles;
-    const int64_t i0 = (rg * 8 + warp) * T;
-    if (i0 >= n1) return;
-    const int64_t a = ct * 32 + lane;
-    const bool aval = a < n2;
-    const int64_t ac = aval ? a : 0;
+    const int ct = blockIdx.x % ncoltiles, rg = blockIdx.x / ncoltiles;
+    const int iblk = rg * ROWS;
+    const int i0 = iblk + warp * T;
+    int acol[CPT];
+    bool aval[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        acol[c] = ct * 32 * CPT + c * 32 + lane;
+        aval[c] = acol[c] < n2;
+        if (!aval[c]) acol[c] = 0;
+    }
     bool anyb = false;
 #pragma unroll
     for (int t = 0; t < T; ++t)
         if (i0 + t < n1) anyb |= xflag[i0 + t] != 0;
-    double acc[SO][T];
+    double acc[SO][T][CPT];
 #pragma unroll
     for (int s = 0; s < SO; ++s)
 #pragma unroll
-        for (int t = 0; t < T; ++t) acc[s][t] = 0.0;
-    const int64_t plane = n1 * n2;
-    for (int e = 0; e < ep.ne; ++e) {
-        if (ep.e[e].bonly && !anyb) continue;
-        const double* Z = ep.e[e].in + (int64_t)ep.e[e].s_in * plane;
-        const double* C = ep.e[e].cst;
-        const int so_ = ep.e[e].s_out;
-        double tmp[T];
+        for (int t = 0; t < T; ++t)
 #pragma unroll
-        for (int t = 0; t < T; ++t) tmp[t] = 0.0;
+            for (int c = 0; c < CPT; ++c) acc[s][t][c] = 0.0;
+    const long long plane = (long long)n1 * n2;
+    for (int e0 = 0; e0 < ep.ne; e0 += XG_ECH) {
+        const int ech = min(XG_ECH, ep.ne - e0);
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < ech * W * ROWS; idx += 256) {
+            const int e = idx / (W * ROWS), rem = idx - e * W * ROWS, k = rem / ROWS, r = rem - k * ROWS;
+            const int i = iblk + r;
+            cs[e][k][r] = i < n1 ? __ldg(ep.e[e0 + e].cst + (long long)k * n1 + i) : 0.0;
+        }
+        __syncthreads();
+        if (i0 >= n1) continue;
+        for (int e = 0; e < ech; ++e) {
+            const XgatEntry& E = ep.e[e0 + e];
+            if (E.bonly && !anyb) continue;
+            const double* Z = E.in + (long long)E.s_in * plane;
+            double tmp[T][CPT];
 #pragma unroll
-        for (int b = 0; b < B::NB; ++b) {
-            constexpr int MAXL = 3;
-            const int klo = B::lo(b), len = B::len(b);
-            const int64_t base = i0 + so.off[klo];
-            double z[T + MAXL - 1];
+            for (int t = 0; t < T; ++t)
 #pragma unroll
-            for (int q = 0; q < T + MAXL - 1; ++q) {
-                if (q < T + len - 1) {
-                    int64_t r = base + q;
-                    r = r < 0 ? 0 : (r >= n1 ? n1 - 1 : r);
-                    z[q] = __ldg(Z + r * n2 + ac);
+                for (int c = 0; c < CPT; ++c) tmp[t][c] = 0.0;
+#pragma unroll
+            for (int b = 0; b < B::NB; ++b) {
+                constexpr int MAXL = 3;
+                const int klo = B::lo(b), len = B::len(b);
+                const int base = i0 + (int)so.off[klo];
+                double z[T + MAXL - 1][CPT];
+#pragma unroll
+                for (int q = 0; q < T + MAXL - 1; ++q) {
+                    if (q < T + len - 1) {
+                        int r = base + q;
+                        r = r < 0 ? 0 : (r >= n1 ? n1 - 1 : r);
+                        const double* zr = Z + (long long)r * n2;
+#pragma unroll
+                        for (int c = 0; c < CPT; ++c) z[q][c] = __ldg(zr + acol[c]);
+                    }
                 }
-            }
 #pragma unroll
-            for (int kk = 0; kk < MAXL; ++kk) {
-                if (kk < len) {
+                for (int kk = 0; kk < MAXL; ++kk) {
+                    if (kk < len) {
 #pragma unroll
-                    for (int t = 0; t < T; ++t) {
-                        const int64_t it = i0 + t < n1 ? i0 + t : n1 - 1;
-                        tmp[t] = fma(__ldg(C + (int64_t)(klo + kk) * n1 + it), z[t + kk], tmp[t]);
+                        for (int t = 0; t < T; ++t) {
+                            const double cf = cs[e][klo + kk][warp * T + t];
+#pragma unroll
+                            for (int c = 0; c < CPT; ++c) tmp[t][c] = fma(cf, z[t + kk][c], tmp[t][c]);
+                        }
                     }
                 }
             }
+#pragma unroll
+            for (int s = 0; s < SO; ++s)
+                if (s == E.s_out)
+#pragma unroll
+                    for (int t = 0; t < T; ++t)
+#pragma unroll
+                        for (int c = 0; c < CPT; ++c) acc[s][t][c] += tmp[t][c];
         }
-#pragma unroll
-        for (int s = 0; s < SO; ++s)
-            if (s == so_)
-#pragma unroll
-                for (int t = 0; t < T; ++t) acc[s][t] += tmp[t];
     }
-    if (!aval) return;
+    if (i0 >= n1) return;
 #pragma unroll
     for (int s = 0; s < SO; ++s)
 #pragma unroll
         for (int t = 0; t < T; ++t) {
             if (i0 + t >= n1) continue;
-            double* y = Y + (int64_t)s * plane + (i0 + t) * n2 + a;
-            *y = beta == 0.0 ? acc[s][t] : fma(beta, *y, acc[s][t]);
+            double* yr = Y + (long long)s * plane + (long long)(i0 + t) * n2;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                if (!aval[c]) continue;
+                double* y = yr + acol[c];
+                *y = beta == 0.0 ? acc[s][t][c] : fma(beta, *y, acc[s][t][c]);
+            }
         }
 }
 
@@ -390,23 +427,23 @@ int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const St
                    const VfanParams& vp, const double* X) {
     const int W = (1 << (d + 1)) - 1;
     const int64_t nrows = (int64_t)S * n1;
-    const int64_t ctiles = (n2 + 63) / 64;
+    const int64_t ctiles = (n2 + VF_TC - 1) / VF_TC;
     // enough blocks to fill the machine, as many rows per block as possible (coefficient reuse)
-    int64_t rchunks = std::max<int64_t>(1, (148 * 4 + ctiles - 1) / ctiles);
-    rchunks = std::min<int64_t>(rchunks, (nrows + 7) / 8);
+    int64_t rchunks = std::max<int64_t>(1, (148 * 6 + ctiles - 1) / ctiles);
+    rchunks = std::min<int64_t>(rchunks, (nrows + 15) / 16);
     rchunks = std::max<int64_t>(rchunks, 1);
     const int64_t rpb = (nrows + rchunks - 1) / rchunks;
-    const size_t smem = sizeof(double) * vp.ng * W * 64;
-    dim3 grid((unsigned)ctiles, (unsigned)rchunks), block(64, 4);
+    const size_t smem = sizeof(double) * vp.ng * W * VF_TC;
+    dim3 grid((unsigned)ctiles, (unsigned)rchunks), block(VF_TC, VF_RL);
     if (d == 1) {
-        cudaFuncSetAttribute(k_vfan_st<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_vfan_st<1, 4><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb);
+        cudaFuncSetAttribute(k_vfan_st<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_vfan_st<1, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb);
     } else if (d == 2) {
-        cudaFuncSetAttribute(k_vfan_st<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_vfan_st<2, 4><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb);
+        cudaFuncSetAttribute(k_vfan_st<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_vfan_st<2, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb);
     } else {
-        cudaFuncSetAttribute(k_vfan_st<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_vfan_st<3, 4><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb);
+        cudaFuncSetAttribute(k_vfan_st<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_vfan_st<3, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb);
     }
     P->launches++;
     SG_CUDA(cudaGetLastError());
@@ -416,15 +453,22 @@ int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const St
 int launch_xgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
                    const uint8_t* xflag, const XgatParams& ep, double* Y, double beta) {
     constexpr int T = 4;
-    const int64_t ctiles = (n2 + 31) / 32;
-    const int64_t rgroups = ((n1 + T - 1) / T + 7) / 8;
+    const int cpt = n2 >= 64 ? 2 : 1;
+    const int64_t ctiles = (n2 + 32 * cpt - 1) / (32 * cpt);
+    const int64_t rgroups = (n1 + 8 * T - 1) / (8 * T);
     const int64_t nb = ctiles * rgroups;
-#define XG(DD, SS) k_xgat_st<DD, T, SS><<<(unsigned)nb, 256, 0, P->stream>>>(n1, n2, so, xflag, ep, Y, beta, ctiles)
-    if (S_out == 1) {
-        if (d == 1) XG(1, 1); else if (d == 2) XG(2, 1); else XG(3, 1);
-    } else {
-        if (d == 1) XG(1, 2); else if (d == 2) XG(2, 2); else XG(3, 2);
+    if (n1 * n2 >= (1LL << 31) || nb >= (1LL << 31)) {
+        set_error("grid too large for 32-bit stencil indexing");
+        return SG_ERR_UNSUPPORTED;
     }
+#define XG(DD, SS, CC) k_xgat_st<DD, T, SS, CC><<<(unsigned)nb, 256, 0, P->stream>>>((int)n1, (int)n2, so, xflag, ep, Y, beta, (int)ctiles)
+#define XGD(SS, CC) do { if (d == 1) XG(1, SS, CC); else if (d == 2) XG(2, SS, CC); else XG(3, SS, CC); } while (0)
+    if (S_out == 1) {
+        if (cpt == 2) XGD(1, 2); else XGD(1, 1);
+    } else {
+        if (cpt == 2) XGD(2, 2); else XGD(2, 1);
+    }
+#undef XGD
 #undef XG
     P->launches++;
     SG_CUDA(cudaGetLastError());
