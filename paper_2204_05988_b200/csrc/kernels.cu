@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(256, 2) k_xgat_st(int n1, int n2, StencilOff s
 #pragma unroll
                     for (int t = 0; t < T; ++t)
 #pragma unroll
-                        for (int c = 0; c < CPT; ++c) acc[s][t][c] += tmp[t][c];
+                        for (int c = 0; c < CPT; ++c) acc[s][t][c] = fma(E.scale, tmp[t][c], acc[s][t][c]);
         }
     }
     if (i0 >= n1) return;
@@ -421,6 +421,50 @@ __global__ void __launch_bounds__(256, 2) k_xgat_st(int n1, int n2, StencilOff s
                 *y = beta == 0.0 ? acc[s][t][c] : fma(beta, *y, acc[s][t][c]);
             }
         }
+}
+
+// v-side gather with time mixing on box v-lattices (cross-grid upper part):
+// Y[s][j][a] = beta*Y + sum_e [s_out=s] scale_e sum_k st_e[k][a] in_e[s_in][j][a + off_k]
+template <int D>
+__global__ void __launch_bounds__(256) k_vgat_st(int S_out, int n1, int n2, StencilOff so, XgatParams ep,
+                                                 double* __restrict__ Y, double beta) {
+    constexpr int W = stc::Bands<D>::W;
+    const long long plane = (long long)n1 * n2;
+    const long long total = plane * S_out;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int s = (int)(t / plane);
+        const long long rc = t - s * plane;
+        const int j = (int)(rc / n2), a = (int)(rc - (long long)j * n2);
+        double acc = 0.0;
+        for (int e = 0; e < ep.ne; ++e) {
+            const XgatEntry& E = ep.e[e];
+            if (E.s_out != s) continue;
+            const double* row = E.in + ((long long)E.s_in * n1 + j) * n2;
+            double a2 = 0.0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                int c = a + (int)so.off[k];
+                c = c < 0 ? 0 : (c >= n2 ? n2 - 1 : c);
+                a2 = fma(__ldg(E.cst + (long long)k * n2 + a), __ldg(row + c), a2);
+            }
+            acc = fma(E.scale, a2, acc);
+        }
+        Y[t] = beta == 0.0 ? acc : fma(beta, Y[t], acc);
+    }
+}
+
+int launch_vgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
+                   const XgatParams& ep, double* Y, double beta) {
+    const int64_t total = (int64_t)S_out * n1 * n2;
+    if (total == 0) return SG_OK;
+    const int g = grid_for(total);
+    if (d == 1) k_vgat_st<1><<<g, 256, 0, P->stream>>>(S_out, (int)n1, (int)n2, so, ep, Y, beta);
+    else if (d == 2) k_vgat_st<2><<<g, 256, 0, P->stream>>>(S_out, (int)n1, (int)n2, so, ep, Y, beta);
+    else k_vgat_st<3><<<g, 256, 0, P->stream>>>(S_out, (int)n1, (int)n2, so, ep, Y, beta);
+    P->launches++;
+    SG_CUDA(cudaGetLastError());
+    return SG_OK;
 }
 
 int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, const uint8_t* xflag,

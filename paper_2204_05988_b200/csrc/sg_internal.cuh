@@ -122,6 +122,7 @@ struct XgatEntry {
     const double* in;
     const double* cst;
     int s_out, s_in, bonly;
+    double scale;
 };
 struct XgatParams {
     int ne;
@@ -196,6 +197,8 @@ int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const St
                    const VfanParams& vp, const double* X);
 int launch_xgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
                    const uint8_t* xflag, const XgatParams& ep, double* Y, double beta);
+int launch_vgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
+                   const XgatParams& ep, double* Y, double beta);
 // solver.cu
 int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y);
 int apply_cross(sg_problem* P, const std::vector<Term>* terms_override, const double* Tb, int S_out, int S_in,
