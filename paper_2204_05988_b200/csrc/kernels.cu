@@ -328,7 +328,10 @@ __global__ void __launch_bounds__(256, 2) k_xgat_st(int n1, int n2, StencilOff s
     constexpr int ROWS = 8 * T;
     __shared__ double cs[XG_ECH][W][ROWS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int ct = blockIdx.x % ncoltiles, rg = blockIdx.x / ncoltiles;
+    // column-tile-major traversal: concurrently resident blocks cover consecutive
+    // row groups of the same columns, so the x-halo rows of Z stay in L2
+    const int rgroups = (n1 + ROWS - 1) / ROWS;
+    const int ct = blockIdx.x / rgroups, rg = blockIdx.x % rgroups;
     const int iblk = rg * ROWS;
     const int i0 = iblk + warp * T;
     int acol[CPT];
