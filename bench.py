@@ -96,6 +96,21 @@ def peaks():
         return {}
 
 
+def combine_ranks(ms, dof, world, device="cpu"):
+    """Replicas-only aggregation: time = max over ranks,
+    work = sum over ranks.  Host logic, tested with gloo on CPU."""
+    if world <= 1:
+        return ms, dof
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms, dof], dtype=torch.float64, device=device)
+    mx = t.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    sm = t.clone()
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    return float(mx[0]), float(sm[1])
+
+
 def cpu_baseline(cfg_name, budget_s=15.0):
     """The oracle (unmodified) timed on the host cores on a bounded sample of the
     same workload: strip-operator applies on the component grids of the same
@@ -191,13 +206,7 @@ def main():
     st = prob.stats()
     kt = prob.kernel_time()
     prob.set_timing(False)
-    if world > 1:
-        t = torch.tensor([ms, float(st["dof_applied"])], dtype=torch.float64, device="cuda")
-        mx = t.clone(); dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = t.clone(); dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        ms_max, dof_all = float(mx[0]), float(sm[1])
-    else:
-        ms_max, dof_all = ms, float(st["dof_applied"])
+    ms_max, dof_all = combine_ranks(ms, float(st["dof_applied"]), world, device="cuda")
     value = dof_all / (ms_max / 1e3)
     # ------------------------------------------------------------- e2e (host buffers)
     e2e = None

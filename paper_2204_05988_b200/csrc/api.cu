@@ -59,6 +59,11 @@ extern "C" int sg_create(const sg_config* cfg, void* stream, sg_problem** out) {
     P->cfg = *cfg;
     P->stream = (cudaStream_t)stream;
     P->verbose = getenv("SG_VERBOSE") != nullptr;
+    P->use_classes = getenv("SG_NO_CLASSES") == nullptr;
+    // the fused whole-x kernel is instruction bound (one load per FMA) and slower than the
+    // two-pass kernels on B200 in round-1 measurements: opt-in only
+    P->force_path = getenv("SG_FUSED") ? 0 : 1;
+    if (getenv("SG_FORCE_2PASS")) P->force_path = 1;
     P->S = cfg->q + 1;
     P->F = cfg->L - 1;
     auto setf = [&](Factor& f, int kind, const double* lo, const double* hi) {
@@ -182,6 +187,7 @@ static void free_level(Level& L) {
     cudaFree(L.bflag);
     for (double* p : L.fm) cudaFree(p);
     for (double* p : L.fst) cudaFree(p);
+    for (double* p : L.fcls) cudaFree(p);
 }
 
 extern "C" void sg_destroy(sg_problem* P) {
@@ -195,12 +201,14 @@ extern "C" void sg_destroy(sg_problem* P) {
                 for (auto& ce : lv) {
                     cudaFree(ce.vals);
                     cudaFree(ce.st);
+                    cudaFree(ce.ctab);
                 }
     cudaFree(P->wsZ); cudaFree(P->wsA); cudaFree(P->wsB); cudaFree(P->red); cudaFree(P->scal);
     if (P->hscal) cudaFreeHost(P->hscal);
     for (double* v : P->vec) cudaFree(v);
     cudaFree(P->trace_dev);
     cudaFree(P->dinv);
+    cudaFree(P->egrp_dev);
     for (auto& pr : P->ev_pairs) {
         cudaEventDestroy(pr.first);
         cudaEventDestroy(pr.second);

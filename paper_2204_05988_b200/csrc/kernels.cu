@@ -322,7 +322,7 @@ constexpr int XG_ECH = 12;   // entries per shared-memory chunk
 template <int D, int T, int SO, int CPT>
 __global__ void __launch_bounds__(256, 2) k_xgat_st(int n1, int n2, StencilOff so, const uint8_t* __restrict__ xflag,
                                                     XgatParams ep, double* __restrict__ Y, double beta,
-                                                    int ncoltiles) {
+                                                    int ncoltiles, int m) {
     using B = stc::Bands<D>;
     constexpr int W = B::W;
     constexpr int ROWS = 8 * T;
@@ -360,7 +360,24 @@ __global__ void __launch_bounds__(256, 2) k_xgat_st(int n1, int n2, StencilOff s
         for (int idx = threadIdx.x; idx < ech * W * ROWS; idx += 256) {
             const int e = idx / (W * ROWS), rem = idx - e * W * ROWS, k = rem / ROWS, r = rem - k * ROWS;
             const int i = iblk + r;
-            cs[e][k][r] = i < n1 ? __ldg(ep.e[e0 + e].cst + (long long)k * n1 + i) : 0.0;
+            const double* ct_ = ep.e[e0 + e].ctab;
+            double v = 0.0;
+            if (i < n1) {
+                if (ct_) {
+                    int z = i, cls = 0, mul = 1;
+#pragma unroll
+                    for (int q = 0; q < D; ++q) {
+                        const int zq = z % m;
+                        z /= m;
+                        cls += mul * (zq == 0 ? 0 : (zq == m - 1 ? 2 : 1));
+                        mul *= 3;
+                    }
+                    v = __ldg(ct_ + cls * W + k);
+                } else {
+                    v = __ldg(ep.e[e0 + e].cst + (long long)k * n1 + i);
+                }
+            }
+            cs[e][k][r] = v;
         }
         __syncthreads();
         if (i0 >= n1) continue;
@@ -428,45 +445,156 @@ __global__ void __launch_bounds__(256, 2) k_xgat_st(int n1, int n2, StencilOff s
 
 // v-side gather with time mixing on box v-lattices (cross-grid upper part):
 // Y[s][j][a] = beta*Y + sum_e [s_out=s] scale_e sum_k st_e[k][a] in_e[s_in][j][a + off_k]
+// Block = 32 columns x 8 row lanes; the block's coefficients (all entries) are
+// staged once in shared memory and reused for every row the block sweeps.
 template <int D>
 __global__ void __launch_bounds__(256) k_vgat_st(int S_out, int n1, int n2, StencilOff so, XgatParams ep,
-                                                 double* __restrict__ Y, double beta) {
+                                                 double* __restrict__ Y, double beta, int rows_per_block) {
     constexpr int W = stc::Bands<D>::W;
-    const long long plane = (long long)n1 * n2;
-    const long long total = plane * S_out;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const int s = (int)(t / plane);
-        const long long rc = t - s * plane;
-        const int j = (int)(rc / n2), a = (int)(rc - (long long)j * n2);
+    extern __shared__ double cs[];   // [ne][W][32]
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int a = blockIdx.x * 32 + tx;
+    const bool aval = a < n2;
+    for (int idx = ty * 32 + tx; idx < ep.ne * W * 32; idx += 256) {
+        const int e = idx / (W * 32), rem = idx - e * W * 32, k = rem >> 5, c = rem & 31;
+        const int ac = blockIdx.x * 32 + c;
+        cs[idx] = ac < n2 ? __ldg(ep.e[e].cst + (long long)k * n2 + ac) : 0.0;
+    }
+    __syncthreads();
+    if (!aval) return;
+    int addr[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        int c = a + (int)so.off[k];
+        addr[k] = c < 0 ? 0 : (c >= n2 ? n2 - 1 : c);
+    }
+    const int R = S_out * n1;
+    const int rb = blockIdx.y * rows_per_block, re = min(R, rb + rows_per_block);
+    for (int r = rb + ty; r < re; r += 8) {
+        const int s = r / n1, j = r - s * n1;
         double acc = 0.0;
         for (int e = 0; e < ep.ne; ++e) {
             const XgatEntry& E = ep.e[e];
             if (E.s_out != s) continue;
             const double* row = E.in + ((long long)E.s_in * n1 + j) * n2;
+            const double* c = cs + e * W * 32 + tx;
             double a2 = 0.0;
 #pragma unroll
-            for (int k = 0; k < W; ++k) {
-                int c = a + (int)so.off[k];
-                c = c < 0 ? 0 : (c >= n2 ? n2 - 1 : c);
-                a2 = fma(__ldg(E.cst + (long long)k * n2 + a), __ldg(row + c), a2);
-            }
+            for (int k = 0; k < W; ++k) a2 = fma(c[k * 32], __ldg(row + addr[k]), a2);
             acc = fma(E.scale, a2, acc);
         }
-        Y[t] = beta == 0.0 ? acc : fma(beta, Y[t], acc);
+        double* y = Y + (long long)r * n2 + a;
+        *y = beta == 0.0 ? acc : fma(beta, *y, acc);
     }
 }
 
 int launch_vgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
                    const XgatParams& ep, double* Y, double beta) {
-    const int64_t total = (int64_t)S_out * n1 * n2;
-    if (total == 0) return SG_OK;
-    const int g = grid_for(total);
-    if (d == 1) k_vgat_st<1><<<g, 256, 0, P->stream>>>(S_out, (int)n1, (int)n2, so, ep, Y, beta);
-    else if (d == 2) k_vgat_st<2><<<g, 256, 0, P->stream>>>(S_out, (int)n1, (int)n2, so, ep, Y, beta);
-    else k_vgat_st<3><<<g, 256, 0, P->stream>>>(S_out, (int)n1, (int)n2, so, ep, Y, beta);
+    const int64_t R = (int64_t)S_out * n1;
+    if (R * n2 == 0 || ep.ne == 0) return SG_OK;
+    const int W = (1 << (d + 1)) - 1;
+    const int64_t ctiles = (n2 + 31) / 32;
+    int64_t rchunks = std::max<int64_t>(1, (148 * 8 + ctiles - 1) / ctiles);
+    rchunks = std::min<int64_t>(rchunks, (R + 7) / 8);
+    rchunks = std::min<int64_t>(std::max<int64_t>(rchunks, 1), 65535);
+    const int rpb = (int)((R + rchunks - 1) / rchunks);
+    const size_t smem = sizeof(double) * ep.ne * W * 32;
+    dim3 grid((unsigned)ctiles, (unsigned)rchunks), block(32, 8);
+#define VG(DD)                                                                                       \
+    do {                                                                                             \
+        cudaFuncSetAttribute(k_vgat_st<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        k_vgat_st<DD><<<grid, block, smem, P->stream>>>(S_out, (int)n1, (int)n2, so, ep, Y, beta, rpb); \
+    } while (0)
+    if (d == 1) VG(1); else if (d == 2) VG(2); else VG(3);
+#undef VG
     P->launches++;
     SG_CUDA(cudaGetLastError());
+    return SG_OK;
+}
+
+// ---- class compression of translation-invariant stencil matrices on box lattices:
+// row i depends only on its boundary class (per axis: low face / interior / high face).
+__global__ void k_class_check(int64_t n, int d, int m, int W, const double* st, const double* tab, double* out2) {
+    __shared__ double sm[2][8];
+    double dev = 0.0, mag = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t z = i;
+        int cls = 0, mul = 1;
+        for (int q = 0; q < d; ++q) {
+            const int zq = (int)(z % m);
+            z /= m;
+            cls += mul * (zq == 0 ? 0 : (zq == m - 1 ? 2 : 1));
+            mul *= 3;
+        }
+        for (int k = 0; k < W; ++k) {
+            const double a = st[k * n + i];
+            dev = fmax(dev, fabs(a - tab[cls * W + k]));
+            mag = fmax(mag, fabs(a));
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+        mag = fmax(mag, __shfl_xor_sync(0xffffffffu, mag, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        sm[0][threadIdx.x >> 5] = dev;
+        sm[1][threadIdx.x >> 5] = mag;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0, b = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            a = fmax(a, sm[0][w]);
+            b = fmax(b, sm[1][w]);
+        }
+        out2[2 * blockIdx.x] = a;
+        out2[2 * blockIdx.x + 1] = b;
+    }
+}
+
+int class_compress(sg_problem* P, const Factor& f, int l, const double* st, double** ctab) {
+    *ctab = nullptr;
+    if (f.kind != SG_MESH_BOX) return SG_OK;
+    const Level& L = f.lev[l];
+    const int d = f.d, W = f.W, m = L.m;
+    int ncls = 1;
+    for (int q = 0; q < d; ++q) ncls *= 3;
+    std::vector<double> tab(27 * W, 0.0);
+    for (int c = 0; c < ncls; ++c) {
+        int cc = c;
+        int64_t idx = 0, mul = 1;
+        for (int q = 0; q < d; ++q) {
+            const int s = cc % 3;
+            cc /= 3;
+            const int z = s == 0 ? 0 : (s == 2 ? m - 1 : (m - 1) / 2);
+            idx += z * mul;
+            mul *= m;
+        }
+        for (int k = 0; k < W; ++k)
+            SG_CUDA(cudaMemcpy(&tab[c * W + k], st + (int64_t)k * L.n + idx, sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    double* dtab;
+    SG_CUDA(cudaMalloc(&dtab, sizeof(double) * 27 * W));
+    SG_CUDA(cudaMemcpy(dtab, tab.data(), sizeof(double) * 27 * W, cudaMemcpyHostToDevice));
+    const int nb = 256;
+    double* out2;
+    SG_CUDA(cudaMalloc(&out2, sizeof(double) * 2 * nb));
+    k_class_check<<<nb, 256, 0, P->stream>>>(L.n, d, m, W, st, dtab, out2);
+    P->launches++;
+    std::vector<double> h(2 * nb);
+    SG_CUDA(cudaMemcpyAsync(h.data(), out2, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost, P->stream));
+    SG_CUDA(cudaStreamSynchronize(P->stream));
+    cudaFree(out2);
+    double dev = 0, mag = 0;
+    for (int b = 0; b < nb; ++b) {
+        dev = std::max(dev, h[2 * b]);
+        mag = std::max(mag, h[2 * b + 1]);
+    }
+    if (dev <= 1e-14 * mag) {
+        *ctab = dtab;
+    } else {
+        cudaFree(dtab);
+    }
     return SG_OK;
 }
 
@@ -498,7 +626,7 @@ int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const St
 }
 
 int launch_xgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
-                   const uint8_t* xflag, const XgatParams& ep, double* Y, double beta) {
+                   const uint8_t* xflag, const XgatParams& ep, double* Y, double beta, int m) {
     constexpr int T = 4;
     const int cpt = n2 >= 64 ? 2 : 1;
     const int64_t ctiles = (n2 + 32 * cpt - 1) / (32 * cpt);
@@ -508,7 +636,7 @@ int launch_xgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, cons
         set_error("grid too large for 32-bit stencil indexing");
         return SG_ERR_UNSUPPORTED;
     }
-#define XG(DD, SS, CC) k_xgat_st<DD, T, SS, CC><<<(unsigned)nb, 256, 0, P->stream>>>((int)n1, (int)n2, so, xflag, ep, Y, beta, (int)ctiles)
+#define XG(DD, SS, CC) k_xgat_st<DD, T, SS, CC><<<(unsigned)nb, 256, 0, P->stream>>>((int)n1, (int)n2, so, xflag, ep, Y, beta, (int)ctiles, m)
 #define XGD(SS, CC) do { if (d == 1) XG(1, SS, CC); else if (d == 2) XG(2, SS, CC); else XG(3, SS, CC); } while (0)
     if (S_out == 1) {
         if (cpt == 2) XGD(1, 2); else XGD(1, 1);
@@ -522,4 +650,138 @@ int launch_xgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, cons
     return SG_OK;
 }
 
+}  // namespace sg
+
+namespace sg {
+// =====================================================================
+// Fused single-pass strip operator for grids whose x factor is small
+// ("whole-x", v-first): one block owns 32 v-columns and ALL S*n1 rows, so the
+// intermediates Z_b = (Id x Id x B_b) X never leave shared memory and X is
+// read once / Y written once (PAPER.md l.516-532 ordering, S^(2) first).
+//   smem: Ysm[S*n1][32] accumulator + Zsm[GC][S*n1][32] for a chunk of GC groups
+// =====================================================================
+constexpr int FW_WARPS = 16;
+template <int DV, int DX>
+__global__ void __launch_bounds__(FW_WARPS * 32, 1) k_fused_wx(int S, int n1, int n2, StencilOff sov, StencilOff sox,
+                                                               int mx, const uint8_t* __restrict__ xflag, VfanParams vp,
+                                                               XgatParams ep, const int* __restrict__ egrp, int GC,
+                                                               const double* __restrict__ X, double* __restrict__ Y) {
+    constexpr int WV = stc::Bands<DV>::W;
+    constexpr int WX = stc::Bands<DX>::W;
+    extern __shared__ double smf[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int R = S * n1;
+    double* Bsm = smf;                                  // [ng][WV][32]
+    double* Ysm = Bsm + (size_t)vp.ng * WV * 32;         // [R][32]
+    double* Zsm = Ysm + (size_t)R * 32;                  // [GC][R][32]
+    const int a = blockIdx.x * 32 + lane;
+    const bool aval = a < n2;
+    for (int idx = threadIdx.x; idx < vp.ng * WV * 32; idx += FW_WARPS * 32) {
+        const int g = idx / (WV * 32), rem = idx - g * WV * 32, k = rem >> 5, c = rem & 31;
+        const int ac = blockIdx.x * 32 + c;
+        Bsm[idx] = ac < n2 ? __ldg(vp.vst[g] + (long long)k * n2 + ac) : 0.0;
+    }
+    int addr[WV];
+#pragma unroll
+    for (int k = 0; k < WV; ++k) {
+        int c = a + (int)sov.off[k];
+        addr[k] = c < 0 ? 0 : (c >= n2 ? n2 - 1 : c);
+    }
+    for (int r = warp; r < R; r += FW_WARPS) Ysm[r * 32 + lane] = 0.0;
+    for (int g0 = 0; g0 < vp.ng; g0 += GC) {
+        const int gc = min(GC, vp.ng - g0);
+        __syncthreads();
+        // stage A: Z_g = B_g X along v for the chunk's groups; X row loaded once per chunk
+        for (int r = warp; r < R; r += FW_WARPS) {
+            const double* xr = X + (long long)r * n2;
+            double x[WV];
+#pragma unroll
+            for (int k = 0; k < WV; ++k) x[k] = aval ? __ldg(xr + addr[k]) : 0.0;
+            const bool bnd = xflag[r % n1] != 0;
+            for (int gi = 0; gi < gc; ++gi) {
+                const int g = g0 + gi;
+                double z = 0.0;
+                if (bnd || g < vp.ng_int) {
+                    const double* Bg = Bsm + (size_t)g * WV * 32 + lane;
+#pragma unroll
+                    for (int k = 0; k < WV; ++k) z = fma(Bg[k * 32], x[k], z);
+                }
+                Zsm[((size_t)gi * R + r) * 32 + lane] = z;
+            }
+        }
+        __syncthreads();
+        // stage B: x-stencil of the chunk's Z into the accumulator
+        for (int r = warp; r < R; r += FW_WARPS) {
+            const int s = r / n1, i = r - s * n1;
+            const bool bnd = xflag[i] != 0;
+            int cls = 0;
+            {
+                int z = i, mul = 1;
+#pragma unroll
+                for (int q = 0; q < DX; ++q) {
+                    const int zq = z % mx;
+                    z /= mx;
+                    cls += mul * (zq == 0 ? 0 : (zq == mx - 1 ? 2 : 1));
+                    mul *= 3;
+                }
+            }
+            int src[WX];
+#pragma unroll
+            for (int k = 0; k < WX; ++k) {
+                int q = i + (int)sox.off[k];
+                src[k] = q < 0 ? 0 : (q >= n1 ? n1 - 1 : q);
+            }
+            double acc = Ysm[r * 32 + lane];
+            for (int e = 0; e < ep.ne; ++e) {
+                const int ge = egrp[e];
+                if (ge < g0 || ge >= g0 + gc) continue;
+                const XgatEntry& E = ep.e[e];
+                if (E.s_out != s || (E.bonly && !bnd)) continue;
+                const double* Zg = Zsm + ((size_t)(ge - g0) * R + (size_t)E.s_in * n1) * 32 + lane;
+                double t = 0.0;
+#pragma unroll
+                for (int k = 0; k < WX; ++k) {
+                    const double cf = E.ctab ? __ldg(E.ctab + cls * WX + k) : __ldg(E.cst + (long long)k * n1 + i);
+                    t = fma(cf, Zg[src[k] * 32], t);
+                }
+                acc = fma(E.scale, t, acc);
+            }
+            Ysm[r * 32 + lane] = acc;
+        }
+    }
+    __syncthreads();
+    if (!aval) return;
+    for (int r = warp; r < R; r += FW_WARPS) Y[(long long)r * n2 + a] = Ysm[r * 32 + lane];
+}
+
+// returns SG_ERR_UNSUPPORTED if the tile does not fit (caller uses the 2-pass path)
+int launch_fused_wx(sg_problem* P, int dv, int dx, int S, int64_t n1, int64_t n2, const StencilOff& sov,
+                    const StencilOff& sox, int mx, const uint8_t* xflag, const VfanParams& vp, const XgatParams& ep,
+                    const int* egrp_dev, const double* X, double* Y) {
+    const size_t row_bytes = (size_t)S * n1 * 32 * sizeof(double);
+    const int WV = (1 << (dv + 1)) - 1;
+    const size_t coef_bytes = (size_t)vp.ng * WV * 32 * sizeof(double);
+    const size_t budget = 220 * 1024;
+    if (coef_bytes + 2 * row_bytes > budget || n1 * n2 >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
+    int GC = (int)((budget - coef_bytes) / row_bytes) - 1;
+    GC = std::max(1, std::min(GC, vp.ng));
+    // many chunks re-read X from L2 each time: prefer the two-pass path then
+    if ((vp.ng + GC - 1) / GC > 4) return SG_ERR_UNSUPPORTED;
+    const size_t smem = coef_bytes + row_bytes * (1 + GC);
+    const unsigned nb = (unsigned)((n2 + 31) / 32);
+#define FW(A, B)                                                                                          \
+    do {                                                                                                  \
+        cudaFuncSetAttribute(k_fused_wx<A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
+        k_fused_wx<A, B><<<nb, FW_WARPS * 32, smem, P->stream>>>(S, (int)n1, (int)n2, sov, sox, mx, xflag, vp, ep, \
+                                                       egrp_dev, GC, X, Y);                               \
+    } while (0)
+    if (dv == 1 && dx == 1) FW(1, 1);
+    else if (dv == 2 && dx == 2) FW(2, 2);
+    else if (dv == 3 && dx == 3) FW(3, 3);
+    else return SG_ERR_UNSUPPORTED;
+#undef FW
+    P->launches++;
+    SG_CUDA(cudaGetLastError());
+    return SG_OK;
+}
 }  // namespace sg

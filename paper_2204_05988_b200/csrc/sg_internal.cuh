@@ -66,6 +66,7 @@ struct Level {
     double* rvals = nullptr;
     std::vector<double*> fm;    // per spec id: [W][n], nullptr if unused
     std::vector<double*> fst;   // per spec id: stencil format [W][n] (box lattices), nullptr if unused
+    std::vector<double*> fcls;  // per spec id: class table [27][W] if translation invariant
     uint8_t* bflag = nullptr;   // 1 for lattice-boundary nodes
     StencilOff so;              // stencil offsets (box lattices)
 };
@@ -103,6 +104,7 @@ struct CombEntry {
     int s_out, s_in;
     double* vals;   // [W][n] device (owned)
     double* st = nullptr;   // stencil format (box lattice of the other factor), owned
+    double* ctab = nullptr; // class table [27][W] if translation invariant, owned
 };
 struct Group {                 // terms sharing one spec on the "inner" factor
     int spec;                  // shared spec id (v-spec for lower/x-groups, x-spec for upper)
@@ -123,6 +125,7 @@ struct XgatEntry {
     const double* cst;
     int s_out, s_in, bonly;
     double scale;
+    const double* ctab = nullptr;   // class-compressed rows [27][W] (translation-invariant matrices) or null
 };
 struct XgatParams {
     int ne;
@@ -169,6 +172,10 @@ struct sg_problem {
     double* trace_dev = nullptr;
     double* dinv = nullptr;                       // block-Jacobi inverse (solve set)
     bool use_precond = true;
+    bool use_classes = true;
+    int force_path = 0;            // 0 auto, 1 two-pass only (tests / experiments)
+    int* egrp_dev = nullptr;       // group index of every diag gather entry (fused kernels)
+    int egrp_n = 0;
     // instrumentation
     int64_t n_applies = 0, dof_applied = 0, launches = 0, outer_iters = 0, inner_iters = 0;
     bool timing = false;
@@ -196,7 +203,11 @@ int launch_ell_to_stencil(sg_problem* P, int64_t n, int W, const int32_t* cols, 
 int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, const uint8_t* xflag,
                    const VfanParams& vp, const double* X);
 int launch_xgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
-                   const uint8_t* xflag, const XgatParams& ep, double* Y, double beta);
+                   const uint8_t* xflag, const XgatParams& ep, double* Y, double beta, int m = 0);
+int class_compress(sg_problem* P, const Factor& f, int l, const double* st, double** ctab);
+int launch_fused_wx(sg_problem* P, int dv, int dx, int S, int64_t n1, int64_t n2, const StencilOff& sov,
+                    const StencilOff& sox, int mx, const uint8_t* xflag, const VfanParams& vp, const XgatParams& ep,
+                    const int* egrp_dev, const double* X, double* Y);
 int launch_vgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
                    const XgatParams& ep, double* Y, double beta);
 // solver.cu

@@ -60,6 +60,43 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
     int64_t l0 = P->launches;
     const bool vbox = P->fv.kind == SG_MESH_BOX && nb <= MAXG;
     const bool xbox = P->fx.kind == SG_MESH_BOX;
+    // ---- fused single pass when the whole x factor of a 32-column tile fits in shared memory
+    if (vbox && xbox && P->force_path != 1) {
+        VfanParams vp;
+        vp.ng = nb;
+        vp.ng_int = P->ng_int;
+        XgatParams ep;
+        ep.ne = 0;
+        std::vector<int> eg;
+        bool fits = true;
+        for (int o = 0; o < nb; ++o) {
+            const Group& gr = P->vgroups[P->vorder[o]];
+            vp.vst[o] = Lv.fst[gr.spec];
+            vp.out[o] = nullptr;
+            for (const auto& ce : gr.comb[g.l1]) {
+                if (ep.ne == MAX_ENTRIES) {
+                    fits = false;
+                    break;
+                }
+                ep.e[ep.ne++] = {nullptr, ce.st, ce.s_out, ce.s_in, gr.bonly ? 1 : 0, 1.0, ce.ctab};
+                eg.push_back(o);
+            }
+        }
+        if (fits && (int)eg.size() == P->egrp_n) {
+            int rc = launch_fused_wx(P, P->fv.d, P->fx.d, S, g.n1, g.n2, Lv.so, Lx.so, Lx.m, Lx.bflag, vp, ep,
+                                     P->egrp_dev, X, Y);
+            if (rc == SG_OK) {
+                P->n_applies++;
+                P->dof_applied += S * n;
+                double bytes = 16.0 * S * n + (8.0 * nb + 4.0) * (double)(P->fv.W * g.n2) +
+                               (8.0 * ep.ne) * (double)(P->fx.W * g.n1);
+                double flops = 2.0 * S * n * ((double)nb * P->fv.W + (double)ep.ne * P->fx.W);
+                SG_TRY(timed_end(P, e0, bytes, flops, (int)(P->launches - l0)));
+                return SG_OK;
+            }
+            if (rc != SG_ERR_UNSUPPORTED) return rc;
+        }
+    }
     // ---- pass 1: Z_b = (Id x Id x B_b) X for every v-group b (interior groups first)
     if (vbox) {
         VfanParams vp;
@@ -91,15 +128,15 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
             const Group& gr = P->vgroups[P->vorder[o]];
             for (const auto& ce : gr.comb[g.l1]) {
                 if (ep.ne == MAX_ENTRIES) {
-                    SG_TRY(launch_xgat_st(P, P->fx.d, S, g.n1, g.n2, Lx.so, Lx.bflag, ep, Y, beta));
+                    SG_TRY(launch_xgat_st(P, P->fx.d, S, g.n1, g.n2, Lx.so, Lx.bflag, ep, Y, beta, Lx.m));
                     beta = 1.0;
                     ep.ne = 0;
                 }
-                ep.e[ep.ne++] = {P->wsZ + (int64_t)o * S * n, ce.st, ce.s_out, ce.s_in, gr.bonly ? 1 : 0, 1.0};
+                ep.e[ep.ne++] = {P->wsZ + (int64_t)o * S * n, ce.st, ce.s_out, ce.s_in, gr.bonly ? 1 : 0, 1.0, ce.ctab};
                 nnz_x++;
             }
         }
-        SG_TRY(launch_xgat_st(P, P->fx.d, S, g.n1, g.n2, Lx.so, Lx.bflag, ep, Y, beta));
+        SG_TRY(launch_xgat_st(P, P->fx.d, S, g.n1, g.n2, Lx.so, Lx.bflag, ep, Y, beta, Lx.m));
     } else {
         EntryList el;
         el.ne = 0;
@@ -194,6 +231,11 @@ int prepare_stencils(sg_problem* P) {
         if (P->fx.kind == SG_MESH_BOX) {
             SG_TRY(ensure_fst(P->fx, P->mass_x, l));
             for (auto& g : P->xgroups) SG_TRY(ensure_fst(P->fx, g.spec, l));
+            Level& L = P->fx.lev[l];
+            L.fcls.assign(P->fx.specs.size(), nullptr);
+            if (P->use_classes)
+                for (size_t sp = 0; sp < P->fx.specs.size(); ++sp)
+                    if (L.fst.size() > sp && L.fst[sp]) SG_TRY(class_compress(P, P->fx, l, L.fst[sp], &L.fcls[sp]));
         }
         if (P->fv.kind == SG_MESH_BOX) {
             SG_TRY(ensure_fst(P->fv, P->mass_v, l));
@@ -220,9 +262,19 @@ int prepare_stencils(sg_problem* P) {
                 for (auto& ce : g.comb[l]) {
                     SG_CUDA(cudaMalloc(&ce.st, sizeof(double) * P->fx.W * L.n));
                     SG_TRY(launch_ell_to_stencil(P, L.n, P->fx.W, L.cols, ce.vals, L.so, ce.st));
+                    if (P->use_classes) SG_TRY(class_compress(P, P->fx, l, ce.st, &ce.ctab));
                 }
             }
         }
+    }
+    // group index of every diagonal gather entry (same on every level)
+    {
+        std::vector<int> eg;
+        for (int o = 0; o < (int)P->vorder.size(); ++o)
+            for (size_t q = 0; q < P->vgroups[P->vorder[o]].comb[1].size(); ++q) eg.push_back(o);
+        P->egrp_n = (int)std::min<size_t>(eg.size(), MAX_ENTRIES);
+        SG_CUDA(cudaMalloc(&P->egrp_dev, sizeof(int) * MAX_ENTRIES));
+        SG_CUDA(cudaMemcpy(P->egrp_dev, eg.data(), sizeof(int) * P->egrp_n, cudaMemcpyHostToDevice));
     }
     SG_CUDA(cudaStreamSynchronize(P->stream));
     return SG_OK;
@@ -322,12 +374,12 @@ int apply_cross(sg_problem* P, const std::vector<Term>* /*unused*/, const double
                     for (int s = 0; s < S_out; ++s)
                         for (int sp = 0; sp < S_in; ++sp)
                             if (Tb[s * S_in + sp] != 0.0)
-                                ep.e[ep.ne++] = {acc, P->fx.lev[p].fst[P->mass_x], s, sp, 0, Tb[s * S_in + sp]};
+                                ep.e[ep.ne++] = {acc, P->fx.lev[p].fst[P->mass_x], s, sp, 0, Tb[s * S_in + sp], P->fx.lev[p].fcls[P->mass_x]};
                 } else {
-                    for (const auto& ce : P->vgroups[b].comb[p]) ep.e[ep.ne++] = {acc, ce.st, ce.s_out, ce.s_in, bo, 1.0};
+                    for (const auto& ce : P->vgroups[b].comb[p]) ep.e[ep.ne++] = {acc, ce.st, ce.s_out, ce.s_in, bo, 1.0, ce.ctab};
                 }
                 if (ep.ne) SG_TRY(launch_xgat_st(P, P->fx.d, S_out, n1(p), n2(lv), P->fx.lev[p].so, P->fx.lev[p].bflag, ep,
-                                                 Y + offOut[p - 1], 1.0));
+                                                 Y + offOut[p - 1], 1.0, P->fx.lev[p].m));
             } else {
                 EntryList el;
                 el.ne = 0;
@@ -367,9 +419,10 @@ int apply_cross(sg_problem* P, const std::vector<Term>* /*unused*/, const double
                 if (xbox) {
                     XgatParams ep;
                     ep.ne = 0;
-                    for (int s = 0; s < S_in; ++s) ep.e[ep.ne++] = {X + offIn[pp - 1], P->fx.lev[pp].fst[xspec], s, s, 0, 1.0};
+                    for (int s = 0; s < S_in; ++s)
+                        ep.e[ep.ne++] = {X + offIn[pp - 1], P->fx.lev[pp].fst[xspec], s, s, 0, 1.0, P->fx.lev[pp].fcls[xspec]};
                     SG_TRY(launch_xgat_st(P, P->fx.d, S_in, n1(pp), n2(lv), P->fx.lev[pp].so, P->fx.lev[pp].bflag, ep,
-                                          P->wsZ + qoff[pp - 1][0], 0.0));
+                                          P->wsZ + qoff[pp - 1][0], 0.0, P->fx.lev[pp].m));
                 } else {
                     FanoutList fl;
                     fl.no = 1;

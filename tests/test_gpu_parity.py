@@ -247,3 +247,67 @@ def test_zero_rhs_gives_zero():
     u = torch.zeros_like(b)
     it, last = g.sg_solve_strip(b, u)
     assert it == 1 and float(u.abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("name", CONFIG_ORDER)
+def test_apply_strip_operator_fused_path(name, monkeypatch):
+    """Same parity with the opt-in fused whole-x kernel enabled (SG_FUSED=1)."""
+    from oracle.sgrid import SGProblem
+    from paper_2204_05988_b200 import Problem
+    monkeypatch.setenv("SG_FUSED", "1")
+    cfg = get_config(name, L=SMALL[name])
+    g, o = Problem(cfg), SGProblem(cfg)
+    rng = np.random.default_rng(5)
+    for set_, grids in ((SET_ACTIVE, o.active), (SET_COARSE, o.coarse)):
+        for gi, l in enumerate(grids):
+            X = rng.standard_normal(o.shape(l))
+            Xt = torch.from_numpy(X.ravel()).cuda()
+            Yt = torch.zeros_like(Xt)
+            g.sg_apply_strip_operator(set_, gi, Xt, Yt)
+            assert relmax(Yt.cpu().numpy().reshape(X.shape), o.apply_diag(l, X)) <= 1e-12, (set_, l)
+
+
+def test_apply_strip_operator_full_size():
+    """configs[4] at its full size (L=8), launch configuration of bench.py.
+    The balanced grid (4,4) (24M DOF, 2-pass kernels) is compared element by
+    element with the oracle (exact factor matrices on its own level-4 meshes);
+    the extreme grid (1,7) (58M DOF, fused kernel) by properties that hold at
+    any size: linearity and 1^T A 1 = |Omega| + tau int_{Gamma^-} |beta.n|
+    (eq. (11) with v = 1: every derivative term vanishes on constants)."""
+    from oracle.sgrid import SGProblem
+    from paper_2204_05988_b200 import Problem
+    cfg = get_config("c4_6d_stream")
+    g = Problem(cfg)
+    rng = np.random.default_rng(9)
+    # --- element-wise on grid (4,4)
+    o = SGProblem(get_config("c4_6d_stream", L=5), galerkin="direct")   # meshes up to level 4
+    o.tau, o.delta = cfg["tau"], g.delta
+    from oracle.problem import strip_terms
+    o.terms = strip_terms(cfg, cfg["tau"], g.delta)
+    l1, l2, n1, n2 = g.grid_info(SET_ACTIVE, 3)
+    assert (l1, l2) == (4, 4)
+    X = rng.standard_normal((1, n1, n2))
+    Yt = torch.empty(n1 * n2, dtype=torch.float64, device="cuda")
+    g.sg_apply_strip_operator(SET_ACTIVE, 3, torch.from_numpy(X.ravel()).cuda(), Yt)
+    ref = o.apply_pair(o.terms, (4, 4), (4, 4), X)
+    assert relmax(Yt.cpu().numpy().reshape(X.shape), ref) <= 1e-12
+    # --- properties on grid (1,7)
+    gi = 0
+    l1, l2, n1, n2 = g.grid_info(SET_ACTIVE, gi)
+    X1 = torch.from_numpy(rng.standard_normal(n1 * n2)).cuda()
+    X2 = torch.from_numpy(rng.standard_normal(n1 * n2)).cuda()
+    Y1, Y2, Y3 = torch.empty_like(X1), torch.empty_like(X1), torch.empty_like(X1)
+    g.sg_apply_strip_operator(SET_ACTIVE, gi, X1, Y1)
+    g.sg_apply_strip_operator(SET_ACTIVE, gi, X2, Y2)
+    g.sg_apply_strip_operator(SET_ACTIVE, gi, (2.0 * X1 - 3.0 * X2).contiguous(), Y3)
+    lin = 2.0 * Y1 - 3.0 * Y2
+    assert float((Y3 - lin).abs().max() / lin.abs().max()) <= 1e-13
+    ones = torch.ones(n1 * n2, dtype=torch.float64, device="cuda")
+    Y = torch.empty_like(ones)
+    g.sg_apply_strip_operator(SET_ACTIVE, gi, ones, Y)
+    # Omega = [0,1]^3 x [-4,4]^3, beta = (v, 0): inflow on x_i = 0 (v_i > 0) and x_i = 1 (v_i < 0),
+    # int_{v_i > 0} v_i dv = 8 * 8 * 8 = 512 per face -> 3 axes * 2 faces * 512
+    tau = cfg["tau"]
+    expect = 512.0 + tau * 3 * 2 * 512.0
+    val = float(Y.sum())
+    assert abs(val - expect) <= 1e-12 * expect, (val, expect)
