@@ -62,8 +62,10 @@ extern "C" int sg_create(const sg_config* cfg, void* stream, sg_problem** out) {
     P->use_classes = getenv("SG_NO_CLASSES") == nullptr;
     // the fused whole-x kernel is instruction bound (one load per FMA) and slower than the
     // two-pass kernels on B200 in round-1 measurements: opt-in only
-    P->force_path = getenv("SG_FUSED") ? 0 : 1;
-    if (getenv("SG_FORCE_2PASS")) P->force_path = 1;
+    P->use_fused = getenv("SG_FUSED") != nullptr;
+    // x-first for n1 > n2 measured slower than v-first on configs[4] (19 vs 10 intermediates):
+    // never by default, SG_XFIRST_AUTO / SG_FORCE_XFIRST opt in
+    P->xfirst_mode = getenv("SG_FORCE_XFIRST") ? 2 : (getenv("SG_XFIRST_AUTO") ? 0 : 1);
     P->S = cfg->q + 1;
     P->F = cfg->L - 1;
     auto setf = [&](Factor& f, int kind, const double* lo, const double* hi) {
@@ -156,7 +158,7 @@ extern "C" int sg_assemble_factors(sg_problem* P) {
         for (int k = 0; k <= ng - pp; ++k) chain += P->fx.lev[pp].n * P->fv.lev[L - pp - k].n;
     for (int pp = 2; pp <= ng; ++pp)
         for (int k = 0; k <= pp - 1; ++k) chain_up += P->fx.lev[pp - k].n * P->fv.lev[L - pp].n;
-    const size_t nbz = std::max(P->vgroups.size(), (size_t)1);
+    const size_t nbz = std::max(std::max(P->vgroups.size(), P->xgroups.size()), (size_t)1);
     P->wsZ_n = (size_t)std::max<int64_t>(std::max<int64_t>(nbz * S * maxg, S * chain), S * chain_up);
     P->wsA_n = P->wsB_n = (size_t)(S * maxg);
     SG_CUDA(cudaMalloc(&P->wsZ, sizeof(double) * P->wsZ_n));

@@ -443,13 +443,131 @@ __global__ void __launch_bounds__(256, 2) k_xgat_st(int n1, int n2, StencilOff s
         }
 }
 
+// x-side fanout (x-first two-pass order for grids with n1 > n2):
+// U_g[s][i][a] = sum_k A_g[i, i + off_k] X[s][i + off_k][a] for all x-groups g.
+// Warp = 32*CPT columns x T consecutive target rows; the X band rows are loaded
+// once and reused for every group; coefficients come from the class tables
+// (translation-invariant x matrices) or the stencil arrays.
+template <int D, int T, int CPT>
+__global__ void __launch_bounds__(256, 2) k_xfan_st(int n1, int n2, StencilOff so, int m, const uint8_t* __restrict__ xflag,
+                                                    XfanParams fp, const double* __restrict__ X, int ncoltiles) {
+    using B = stc::Bands<D>;
+    constexpr int W = B::W;
+    constexpr int ROWS = 8 * T;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int rgroups = (n1 + ROWS - 1) / ROWS;
+    const int s = blockIdx.y;
+    const int ct = blockIdx.x / rgroups, rg = blockIdx.x % rgroups;
+    const int i0 = rg * ROWS + warp * T;
+    if (i0 >= n1) return;
+    const long long plane = (long long)n1 * n2;
+    const double* Xs = X + s * plane;
+    int acol[CPT];
+    bool aval[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        acol[c] = ct * 32 * CPT + c * 32 + lane;
+        aval[c] = acol[c] < n2;
+        if (!aval[c]) acol[c] = 0;
+    }
+    bool anyb = false;
+    int cls[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        const int it = min(i0 + t, n1 - 1);
+        anyb |= (i0 + t < n1) && xflag[it] != 0;
+        int z = it, cl = 0, mul = 1;
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+            const int zq = z % m;
+            z /= m;
+            cl += mul * (zq == 0 ? 0 : (zq == m - 1 ? 2 : 1));
+            mul *= 3;
+        }
+        cls[t] = cl;
+    }
+    constexpr int MAXL = 3;
+    double z[B::NB][T + MAXL - 1][CPT];
+#pragma unroll
+    for (int b = 0; b < B::NB; ++b) {
+        const int klo = B::lo(b), len = B::len(b);
+        const int base = i0 + (int)so.off[klo];
+#pragma unroll
+        for (int q = 0; q < T + MAXL - 1; ++q) {
+            if (q < T + len - 1) {
+                int r = base + q;
+                r = r < 0 ? 0 : (r >= n1 ? n1 - 1 : r);
+                const double* zr = Xs + (long long)r * n2;
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) z[b][q][c] = __ldg(zr + acol[c]);
+            }
+        }
+    }
+    const int ngu = anyb ? fp.ng : fp.ng_int;
+    for (int g = 0; g < ngu; ++g) {
+        const double* tab = fp.ctab[g];
+        const double* st = fp.cst[g];
+        double acc[T][CPT];
+#pragma unroll
+        for (int t = 0; t < T; ++t)
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) acc[t][c] = 0.0;
+#pragma unroll
+        for (int b = 0; b < B::NB; ++b) {
+            const int klo = B::lo(b), len = B::len(b);
+#pragma unroll
+            for (int kk = 0; kk < MAXL; ++kk) {
+                if (kk < len) {
+#pragma unroll
+                    for (int t = 0; t < T; ++t) {
+                        const int it = min(i0 + t, n1 - 1);
+                        const double cf = tab ? __ldg(tab + cls[t] * W + klo + kk) : __ldg(st + (long long)(klo + kk) * n1 + it);
+#pragma unroll
+                        for (int c = 0; c < CPT; ++c) acc[t][c] = fma(cf, z[b][t + kk][c], acc[t][c]);
+                    }
+                }
+            }
+        }
+        double* o = fp.out[g] + s * plane;
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+            if (i0 + t >= n1) continue;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c)
+                if (aval[c]) o[(long long)(i0 + t) * n2 + acol[c]] = acc[t][c];
+        }
+    }
+}
+
+int launch_xfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, int m,
+                   const uint8_t* xflag, const XfanParams& fp, const double* X) {
+    constexpr int T = 4;
+    const int cpt = n2 >= 64 ? 2 : 1;
+    const int64_t ctiles = (n2 + 32 * cpt - 1) / (32 * cpt);
+    const int64_t rgroups = (n1 + 8 * T - 1) / (8 * T);
+    const int64_t nb = ctiles * rgroups;
+    if (n1 * n2 >= (1LL << 31) || nb >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
+    dim3 grid((unsigned)nb, (unsigned)S);
+#define XF(DD, CC) k_xfan_st<DD, T, CC><<<grid, 256, 0, P->stream>>>((int)n1, (int)n2, so, m, xflag, fp, X, (int)ctiles)
+    if (cpt == 2) {
+        if (d == 1) XF(1, 2); else if (d == 2) XF(2, 2); else XF(3, 2);
+    } else {
+        if (d == 1) XF(1, 1); else if (d == 2) XF(2, 1); else XF(3, 1);
+    }
+#undef XF
+    P->launches++;
+    SG_CUDA(cudaGetLastError());
+    return SG_OK;
+}
+
 // v-side gather with time mixing on box v-lattices (cross-grid upper part):
 // Y[s][j][a] = beta*Y + sum_e [s_out=s] scale_e sum_k st_e[k][a] in_e[s_in][j][a + off_k]
 // Block = 32 columns x 8 row lanes; the block's coefficients (all entries) are
 // staged once in shared memory and reused for every row the block sweeps.
 template <int D>
 __global__ void __launch_bounds__(256) k_vgat_st(int S_out, int n1, int n2, StencilOff so, XgatParams ep,
-                                                 double* __restrict__ Y, double beta, int rows_per_block) {
+                                                 double* __restrict__ Y, double beta, int rows_per_block,
+                                                 const uint8_t* __restrict__ xflag) {
     constexpr int W = stc::Bands<D>::W;
     extern __shared__ double cs[];   // [ne][W][32]
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -472,10 +590,11 @@ __global__ void __launch_bounds__(256) k_vgat_st(int S_out, int n1, int n2, Sten
     const int rb = blockIdx.y * rows_per_block, re = min(R, rb + rows_per_block);
     for (int r = rb + ty; r < re; r += 8) {
         const int s = r / n1, j = r - s * n1;
+        const bool bnd = xflag == nullptr || xflag[j] != 0;
         double acc = 0.0;
         for (int e = 0; e < ep.ne; ++e) {
             const XgatEntry& E = ep.e[e];
-            if (E.s_out != s) continue;
+            if (E.s_out != s || (E.bonly && !bnd)) continue;
             const double* row = E.in + ((long long)E.s_in * n1 + j) * n2;
             const double* c = cs + e * W * 32 + tx;
             double a2 = 0.0;
@@ -489,7 +608,7 @@ __global__ void __launch_bounds__(256) k_vgat_st(int S_out, int n1, int n2, Sten
 }
 
 int launch_vgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
-                   const XgatParams& ep, double* Y, double beta) {
+                   const XgatParams& ep, double* Y, double beta, const uint8_t* xflag) {
     const int64_t R = (int64_t)S_out * n1;
     if (R * n2 == 0 || ep.ne == 0) return SG_OK;
     const int W = (1 << (d + 1)) - 1;
@@ -503,7 +622,7 @@ int launch_vgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, cons
 #define VG(DD)                                                                                       \
     do {                                                                                             \
         cudaFuncSetAttribute(k_vgat_st<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-        k_vgat_st<DD><<<grid, block, smem, P->stream>>>(S_out, (int)n1, (int)n2, so, ep, Y, beta, rpb); \
+        k_vgat_st<DD><<<grid, block, smem, P->stream>>>(S_out, (int)n1, (int)n2, so, ep, Y, beta, rpb, xflag); \
     } while (0)
     if (d == 1) VG(1); else if (d == 2) VG(2); else VG(3);
 #undef VG

@@ -127,6 +127,12 @@ struct XgatEntry {
     double scale;
     const double* ctab = nullptr;   // class-compressed rows [27][W] (translation-invariant matrices) or null
 };
+struct XfanParams {
+    int ng, ng_int;
+    const double* cst[MAXG];
+    const double* ctab[MAXG];
+    double* out[MAXG];
+};
 struct XgatParams {
     int ne;
     XgatEntry e[MAX_ENTRIES];
@@ -158,6 +164,8 @@ struct sg_problem {
     std::vector<sg::Group> xgroups; // grouped by x-spec; comb = v-matrices (upper part)
     int mass_x = -1, mass_v = -1;   // spec ids of the unweighted mass
     std::vector<int> vorder;        // v-groups, interior first then boundary-only
+    std::vector<int> xorder;        // x-groups, interior first then boundary-only
+    int nxg_int = 0;
     int ng_int = 0;
     std::vector<sg::Grid> active, coarse;
     bool meshes_built = false, assembled = false;
@@ -173,7 +181,8 @@ struct sg_problem {
     double* dinv = nullptr;                       // block-Jacobi inverse (solve set)
     bool use_precond = true;
     bool use_classes = true;
-    int force_path = 0;            // 0 auto, 1 two-pass only (tests / experiments)
+    bool use_fused = false;        // opt-in fused whole-x kernel (SG_FUSED)
+    int xfirst_mode = 0;           // 0 auto (n1 > n2), 1 never, 2 always (tests)
     int* egrp_dev = nullptr;       // group index of every diag gather entry (fused kernels)
     int egrp_n = 0;
     // instrumentation
@@ -209,7 +218,9 @@ int launch_fused_wx(sg_problem* P, int dv, int dx, int S, int64_t n1, int64_t n2
                     const StencilOff& sox, int mx, const uint8_t* xflag, const VfanParams& vp, const XgatParams& ep,
                     const int* egrp_dev, const double* X, double* Y);
 int launch_vgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
-                   const XgatParams& ep, double* Y, double beta);
+                   const XgatParams& ep, double* Y, double beta, const uint8_t* xflag = nullptr);
+int launch_xfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, int m,
+                   const uint8_t* xflag, const XfanParams& fp, const double* X);
 // solver.cu
 int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y);
 int apply_cross(sg_problem* P, const std::vector<Term>* terms_override, const double* Tb, int S_out, int S_in,

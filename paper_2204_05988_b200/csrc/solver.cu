@@ -61,7 +61,7 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
     const bool vbox = P->fv.kind == SG_MESH_BOX && nb <= MAXG;
     const bool xbox = P->fx.kind == SG_MESH_BOX;
     // ---- fused single pass when the whole x factor of a 32-column tile fits in shared memory
-    if (vbox && xbox && P->force_path != 1) {
+    if (vbox && xbox && P->use_fused) {
         VfanParams vp;
         vp.ng = nb;
         vp.ng_int = P->ng_int;
@@ -91,6 +91,49 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
                 double bytes = 16.0 * S * n + (8.0 * nb + 4.0) * (double)(P->fv.W * g.n2) +
                                (8.0 * ep.ne) * (double)(P->fx.W * g.n1);
                 double flops = 2.0 * S * n * ((double)nb * P->fv.W + (double)ep.ne * P->fx.W);
+                SG_TRY(timed_end(P, e0, bytes, flops, (int)(P->launches - l0)));
+                return SG_OK;
+            }
+            if (rc != SG_ERR_UNSUPPORTED) return rc;
+        }
+    }
+    // ---- x-first two-pass order for grids with a large x and a small v factor:
+    // U_a = (Id x A_a x Id) X for every x-group a, then Y = sum_a (Id x D_a) U_a along v.
+    // The x-halo (lexicographic offsets up to m^2 rows) then falls on the single
+    // input X instead of on every intermediate.
+    const int nxg = (int)P->xorder.size();
+    if (vbox && xbox && nxg <= MAXG && (size_t)nxg * S * n <= P->wsZ_n &&
+        (P->xfirst_mode == 2 || (P->xfirst_mode == 0 && g.n1 > g.n2))) {
+        XfanParams fp;
+        fp.ng = nxg;
+        fp.ng_int = P->nxg_int;
+        int64_t nnz_e = 0;
+        XgatParams ep;
+        ep.ne = 0;
+        bool fits = true;
+        for (int o = 0; o < nxg; ++o) {
+            const Group& gr = P->xgroups[P->xorder[o]];
+            fp.cst[o] = Lx.fst[gr.spec];
+            fp.ctab[o] = Lx.fcls.size() > (size_t)gr.spec ? Lx.fcls[gr.spec] : nullptr;
+            fp.out[o] = P->wsZ + (int64_t)o * S * n;
+            for (const auto& ce : gr.comb[g.l2]) {
+                if (ep.ne == MAX_ENTRIES) {
+                    fits = false;
+                    break;
+                }
+                ep.e[ep.ne++] = {fp.out[o], ce.st, ce.s_out, ce.s_in, gr.bonly ? 1 : 0, 1.0, nullptr};
+                nnz_e++;
+            }
+        }
+        if (fits) {
+            int rc = launch_xfan_st(P, P->fx.d, S, g.n1, g.n2, Lx.so, Lx.m, Lx.bflag, fp, X);
+            if (rc == SG_OK) {
+                SG_TRY(launch_vgat_st(P, P->fv.d, S, g.n1, g.n2, Lv.so, ep, Y, 0.0, Lx.bflag));
+                P->n_applies++;
+                P->dof_applied += S * n;
+                double bytes = 16.0 * S * n + (8.0 * nnz_e + 4.0) * (double)(P->fv.W * g.n2) +
+                               (8.0 * nxg + 4.0) * (double)(P->fx.W * g.n1);
+                double flops = 2.0 * S * n * ((double)nxg * P->fx.W + (double)nnz_e * P->fv.W);
                 SG_TRY(timed_end(P, e0, bytes, flops, (int)(P->launches - l0)));
                 return SG_OK;
             }
@@ -212,11 +255,17 @@ int prepare_stencils(sg_problem* P) {
         }
     P->ng_int = 0;
     for (int gi : P->vorder) P->ng_int += P->vgroups[gi].bonly ? 0 : 1;
-    for (auto& g : P->xgroups) {
-        bool bonly = true;
-        for (int t : g.terms) bonly &= P->fv.specs[P->terms[t].vs].kind == 1;
-        g.bonly = bonly;
-    }
+    // x-groups: "boundary-only" means the x matrix is a face mass (nonzero on boundary x-rows only)
+    P->xorder.clear();
+    for (int pass = 0; pass < 2; ++pass)
+        for (size_t gi = 0; gi < P->xgroups.size(); ++gi) {
+            Group& g = P->xgroups[gi];
+            const bool bonly = P->fx.specs[g.spec].kind == 1;
+            g.bonly = bonly;
+            if ((pass == 0) != bonly) P->xorder.push_back((int)gi);
+        }
+    P->nxg_int = 0;
+    for (int gi : P->xorder) P->nxg_int += P->xgroups[gi].bonly ? 0 : 1;
     // stencil-format copies
     auto ensure_fst = [&](Factor& f, int spec, int l) -> int {
         Level& L = f.lev[l];

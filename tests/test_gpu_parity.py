@@ -249,12 +249,15 @@ def test_zero_rhs_gives_zero():
     assert it == 1 and float(u.abs().max()) == 0.0
 
 
+@pytest.mark.parametrize("env", ["SG_FUSED", "SG_NO_XFIRST", "SG_FORCE_XFIRST"])
 @pytest.mark.parametrize("name", CONFIG_ORDER)
-def test_apply_strip_operator_fused_path(name, monkeypatch):
-    """Same parity with the opt-in fused whole-x kernel enabled (SG_FUSED=1)."""
+def test_apply_strip_operator_kernel_paths(name, env, monkeypatch):
+    """Same parity on every kernel path at test sizes: the opt-in fused whole-x
+    kernel, the v-first two-pass kernels everywhere, the x-first two-pass kernels
+    everywhere (large grids pick v-first or x-first by shape)."""
     from oracle.sgrid import SGProblem
     from paper_2204_05988_b200 import Problem
-    monkeypatch.setenv("SG_FUSED", "1")
+    monkeypatch.setenv(env, "1")
     cfg = get_config(name, L=SMALL[name])
     g, o = Problem(cfg), SGProblem(cfg)
     rng = np.random.default_rng(5)
