@@ -63,6 +63,14 @@ extern "C" int sg_create(const sg_config* cfg, void* stream, sg_problem** out) {
     // the fused whole-x kernel is instruction bound (one load per FMA) and slower than the
     // two-pass kernels on B200 in round-1 measurements: opt-in only
     P->use_fused = getenv("SG_FUSED") != nullptr;
+    P->use_graphs = getenv("SG_NO_GRAPHS") == nullptr;
+    if (cudaStreamCreateWithFlags(&P->gstream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&P->ev_a, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&P->ev_b, cudaEventDisableTiming) != cudaSuccess) {
+        set_error("stream/event creation failed");
+        delete P;
+        return SG_ERR_CUDA;
+    }
     // x-first for n1 > n2 measured slower than v-first on configs[4] (19 vs 10 intermediates):
     // never by default, SG_XFIRST_AUTO / SG_FORCE_XFIRST opt in
     P->xfirst_mode = getenv("SG_FORCE_XFIRST") ? 2 : (getenv("SG_XFIRST_AUTO") ? 0 : 1);
@@ -211,6 +219,10 @@ extern "C" void sg_destroy(sg_problem* P) {
     cudaFree(P->trace_dev);
     cudaFree(P->dinv);
     cudaFree(P->egrp_dev);
+    for (auto& g : P->graphs) cudaGraphExecDestroy(g.exec);
+    if (P->gstream) cudaStreamDestroy(P->gstream);
+    if (P->ev_a) cudaEventDestroy(P->ev_a);
+    if (P->ev_b) cudaEventDestroy(P->ev_b);
     for (auto& pr : P->ev_pairs) {
         cudaEventDestroy(pr.first);
         cudaEventDestroy(pr.second);

@@ -138,6 +138,25 @@ struct XgatParams {
     XgatEntry e[MAX_ENTRIES];
 };
 
+struct GraphKey {
+    const double* X;
+    double* Y;
+    int S_out, S_in;
+    bool mass;
+    double T[4];
+    bool same(const GraphKey& o) const {
+        if (X != o.X || Y != o.Y || S_out != o.S_out || S_in != o.S_in || mass != o.mass) return false;
+        for (int i = 0; i < 4; ++i)
+            if (T[i] != o.T[i]) return false;
+        return true;
+    }
+};
+struct GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec;
+    int64_t nlaunch;
+};
+
 struct Grid {
     int l1, l2;
     int64_t n1, n2;
@@ -181,6 +200,10 @@ struct sg_problem {
     double* dinv = nullptr;                       // block-Jacobi inverse (solve set)
     bool use_precond = true;
     bool use_classes = true;
+    bool use_graphs = true;
+    cudaStream_t gstream = nullptr;   // library stream for captured graphs
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+    std::vector<sg::GraphEntry> graphs;
     bool use_fused = false;        // opt-in fused whole-x kernel (SG_FUSED)
     int xfirst_mode = 0;           // 0 auto (n1 > n2), 1 never, 2 always (tests)
     int* egrp_dev = nullptr;       // group index of every diag gather entry (fused kernels)

@@ -339,8 +339,61 @@ int prepare_stencils(sg_problem* P) {
 //    gather with the group's combined x matrices;
 //  upper part (l1 < l1'): per x-group a symmetric with the roles of x, v swapped.
 // "mass" mode (Tb != nullptr): single term Tb (x) M^x (x) M^v, S_out x S_in.
+static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in, const double* X, double* Y);
+
+// The cross-grid apply is a fixed sequence of ~10^3 small launches (transfer
+// chains per group); it is captured once per (X, Y, Tb) into a CUDA graph on the
+// library's own stream and replayed, which removes the per-launch CPU cost
+// (dominant on the 2D configurations).
 int apply_cross(sg_problem* P, const std::vector<Term>* /*unused*/, const double* Tb, int S_out, int S_in,
                 const double* X, double* Y) {
+    if (!P->use_graphs) return apply_cross_impl(P, Tb, S_out, S_in, X, Y);
+    GraphKey key;
+    key.X = X;
+    key.Y = Y;
+    key.S_out = S_out;
+    key.S_in = S_in;
+    key.mass = Tb != nullptr;
+    for (int i = 0; i < 4; ++i) key.T[i] = (Tb && i < S_out * S_in) ? Tb[i] : 0.0;
+    GraphEntry* ge = nullptr;
+    for (auto& e : P->graphs)
+        if (e.key.same(key)) ge = &e;
+    cudaStream_t gs = P->gstream;
+    if (!ge) {
+        if (P->graphs.size() >= 24) {
+            cudaGraphExecDestroy(P->graphs.front().exec);
+            P->graphs.erase(P->graphs.begin());
+        }
+        const int64_t l0 = P->launches;
+        cudaStream_t saved = P->stream;
+        P->stream = gs;
+        SG_CUDA(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
+        int rc = apply_cross_impl(P, Tb, S_out, S_in, X, Y);
+        cudaGraph_t graph;
+        cudaError_t ce = cudaStreamEndCapture(gs, &graph);
+        P->stream = saved;
+        if (rc != SG_OK) return rc;
+        SG_CUDA(ce);
+        GraphEntry e;
+        e.key = key;
+        e.nlaunch = P->launches - l0;
+        P->launches = l0;
+        SG_CUDA(cudaGraphInstantiate(&e.exec, graph, 0));
+        cudaGraphDestroy(graph);
+        P->graphs.push_back(e);
+        ge = &P->graphs.back();
+    }
+    // order: user stream -> graph stream -> user stream
+    SG_CUDA(cudaEventRecord(P->ev_a, P->stream));
+    SG_CUDA(cudaStreamWaitEvent(gs, P->ev_a, 0));
+    SG_CUDA(cudaGraphLaunch(ge->exec, gs));
+    SG_CUDA(cudaEventRecord(P->ev_b, gs));
+    SG_CUDA(cudaStreamWaitEvent(P->stream, P->ev_b, 0));
+    P->launches += ge->nlaunch;
+    return SG_OK;
+}
+
+static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in, const double* X, double* Y) {
     const bool mass = Tb != nullptr;
     const auto& A = P->active;
     const int ng = (int)A.size();
