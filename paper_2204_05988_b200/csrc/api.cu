@@ -173,6 +173,7 @@ extern "C" int sg_assemble_factors(sg_problem* P) {
     SG_CUDA(cudaMemsetAsync(P->wsZ, 0, sizeof(double) * P->wsZ_n, P->stream));   // finite garbage only
     SG_CUDA(cudaMalloc(&P->wsA, sizeof(double) * P->wsA_n));
     SG_CUDA(cudaMalloc(&P->wsB, sizeof(double) * P->wsB_n));
+    SG_CUDA(cudaMalloc(&P->wsH, sizeof(double) * 2 * set_size(P, SG_SET_ACTIVE, S)));
     const int64_t Na = set_size(P, SG_SET_ACTIVE, S), Nc = set_size(P, SG_SET_COARSE, S);
     const int64_t nblk = (Na + Nc) / 2048 + 2 * MAX_SEG + 8;
     SG_CUDA(cudaMalloc(&P->red, sizeof(double) * 3 * nblk));
@@ -213,7 +214,7 @@ extern "C" void sg_destroy(sg_problem* P) {
                     cudaFree(ce.st);
                     cudaFree(ce.ctab);
                 }
-    cudaFree(P->wsZ); cudaFree(P->wsA); cudaFree(P->wsB); cudaFree(P->red); cudaFree(P->scal);
+    cudaFree(P->wsZ); cudaFree(P->wsA); cudaFree(P->wsB); cudaFree(P->wsH); cudaFree(P->red); cudaFree(P->scal);
     if (P->hscal) cudaFreeHost(P->hscal);
     for (double* v : P->vec) cudaFree(v);
     cudaFree(P->trace_dev);

@@ -904,3 +904,64 @@ int launch_fused_wx(sg_problem* P, int dv, int dx, int S, int64_t n1, int64_t n2
     return SG_OK;
 }
 }  // namespace sg
+
+namespace sg {
+// =====================================================================
+// Batched transfer jobs: independent Kronecker-factored ELL applies (the
+// restriction / prolongation chains of the cross-grid apply) in ONE launch.
+//   out[t] = (add ? add[t] : 0) + scale * sum_k M[k][row] * in[... col_k ...]
+// Block b serves job j with blk0[j] <= b < blk0[j+1].
+// =====================================================================
+__global__ void __launch_bounds__(256) k_jobs(JobList jl) {
+    int j = 0;
+    while (j + 1 < jl.nj && jl.j[j + 1].blk0 <= (int)blockIdx.x) ++j;
+    const Job& J = jl.j[j];
+    const int64_t n1_out = J.dir == 0 ? J.nrows_out : J.n1_in;
+    const int64_t n2_out = J.dir == 1 ? J.nrows_out : J.n2_in;
+    const int64_t per_s = n1_out * n2_out;
+    const int64_t total = per_s * J.S;
+    const int nblk = (j + 1 < jl.nj ? jl.j[j + 1].blk0 : jl.total_blocks) - J.blk0;
+    for (int64_t t = (int64_t)(blockIdx.x - J.blk0) * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)nblk * blockDim.x) {
+        const int s = (int)(t / per_s);
+        const int64_t rc = t - s * per_s;
+        const int64_t r = rc / n2_out, c = rc - r * n2_out;
+        const int64_t row = J.dir == 1 ? c : r;
+        const int64_t nrows = J.nrows_out;
+        double acc = 0.0;
+        for (int k = 0; k < J.W; ++k) {
+            const int32_t col = __ldg(J.cols + k * nrows + row);
+            if (col < 0) continue;
+            const double x = J.dir == 1 ? __ldg(J.in + ((int64_t)s * J.n1_in + r) * J.n2_in + col)
+                                        : __ldg(J.in + ((int64_t)s * J.n1_in + col) * J.n2_in + c);
+            acc = fma(__ldg(J.vals + k * nrows + row), x, acc);
+        }
+        J.out[t] = (J.add ? J.add[t] : 0.0) + J.scale * acc;
+    }
+}
+
+int launch_jobs(sg_problem* P, std::vector<Job>& jobs) {
+    size_t i = 0;
+    while (i < jobs.size()) {
+        JobList jl;
+        jl.nj = 0;
+        int blk = 0;
+        while (i < jobs.size() && jl.nj < MAX_JOBS) {
+            Job J = jobs[i++];
+            const int64_t n1_out = J.dir == 0 ? J.nrows_out : J.n1_in;
+            const int64_t n2_out = J.dir == 1 ? J.nrows_out : J.n2_in;
+            const int64_t total = n1_out * n2_out * J.S;
+            if (total == 0) continue;
+            J.blk0 = blk;
+            blk += (int)std::min<int64_t>((total + 2047) / 2048, 148 * 8);
+            jl.j[jl.nj++] = J;
+        }
+        if (jl.nj == 0) continue;
+        jl.total_blocks = blk;
+        k_jobs<<<blk, 256, 0, P->stream>>>(jl);
+        P->launches++;
+        SG_CUDA(cudaGetLastError());
+    }
+    return SG_OK;
+}
+}  // namespace sg

@@ -138,6 +138,22 @@ struct XgatParams {
     XgatEntry e[MAX_ENTRIES];
 };
 
+constexpr int MAX_JOBS = 36;
+struct Job {
+    const double* in;
+    const double* add;
+    double* out;
+    const int32_t* cols;
+    const double* vals;
+    int64_t n1_in, n2_in, nrows_out;
+    double scale;
+    int S, dir, W, blk0;
+};
+struct JobList {
+    int nj, total_blocks;
+    Job j[MAX_JOBS];
+};
+
 struct GraphKey {
     const double* X;
     double* Y;
@@ -192,6 +208,7 @@ struct sg_problem {
     double* wsZ = nullptr; size_t wsZ_n = 0;      // fanout outputs / chain buffers
     double* wsA = nullptr; size_t wsA_n = 0;      // Horner ping
     double* wsB = nullptr; size_t wsB_n = 0;      // Horner pong
+    double* wsH = nullptr;                        // per-target Horner buffers [2][active S-set]
     double* red = nullptr;                        // reduction partials
     double* scal = nullptr;                       // per-grid scalars (BiCGStab)
     double* hscal = nullptr;                      // pinned host copy
@@ -237,6 +254,7 @@ int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const St
 int launch_xgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
                    const uint8_t* xflag, const XgatParams& ep, double* Y, double beta, int m = 0);
 int class_compress(sg_problem* P, const Factor& f, int l, const double* st, double** ctab);
+int launch_jobs(sg_problem* P, std::vector<Job>& jobs);
 int launch_fused_wx(sg_problem* P, int dv, int dx, int S, int64_t n1, int64_t n2, const StencilOff& sov,
                     const StencilOff& sox, int mx, const uint8_t* xflag, const VfanParams& vp, const XgatParams& ep,
                     const int* egrp_dev, const double* X, double* Y);

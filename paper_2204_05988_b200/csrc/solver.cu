@@ -443,31 +443,33 @@ static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in
                 fl.out[0] = P->wsZ + qoff[pp - 1][0];
                 SG_TRY(launch_fanout(P, 1, Wv, S_in, n1(lx), n2(lv0), n2(lv0), P->fv.lev[lv0].cols, X + offIn[pp - 1], fl));
             }
-            for (int k = 1; k <= ng - pp; ++k) {
-                const int lf = lv0 - k + 1, lc = lv0 - k;
-                EntryList el;
-                el.ne = 0;
-                for (int s = 0; s < S_in; ++s)
-                    el.e[el.ne++] = {P->wsZ + qoff[pp - 1][k - 1], P->fv.lev[lf].rvals, 1.0, s, s};
-                SG_TRY(launch_gather(P, 1, Wv, S_in, n1(lx), n2(lf), n2(lc), P->fv.lev[lf].rcols, el,
-                                     P->wsZ + qoff[pp - 1][k], 0.0));
+        }
+        // restriction chains in v, batched over sources: stage k maps Q[p'][k-1] -> Q[p'][k]
+        for (int k = 1; k <= ng - 1; ++k) {
+            std::vector<Job> jobs;
+            for (int pp = 1; pp <= ng - k; ++pp) {
+                const int lv0 = L - pp, lf = lv0 - k + 1, lc = lv0 - k;
+                jobs.push_back({P->wsZ + qoff[pp - 1][k - 1], nullptr, P->wsZ + qoff[pp - 1][k], P->fv.lev[lf].rcols,
+                                P->fv.lev[lf].rvals, n1(pp), n2(lf), n2(lc), 1.0, S_in, 1, Wv, 0});
             }
+            SG_TRY(launch_jobs(P, jobs));
+        }
+        // Horner prolongation in x, batched over targets: stage m lifts every target p >= m
+        // from x-level m-1 to m and adds Q[m][p-m]
+        double* hb[2] = {P->wsH, P->wsH + set_size(P, SG_SET_ACTIVE, S_in)};
+        for (int m = 2; m <= ng; ++m) {
+            std::vector<Job> jobs;
+            for (int p = m; p <= ng; ++p) {
+                const int lv = L - p;
+                const double* in = m == 2 ? P->wsZ + qoff[0][p - 1] : hb[(m - 1) & 1] + offIn[p - 1];
+                jobs.push_back({in, P->wsZ + qoff[m - 1][p - m], hb[m & 1] + offIn[p - 1], P->fx.lev[m].pcols,
+                                P->fx.lev[m].pvals, n1(m - 1), n2(lv), n1(m), 1.0, S_in, 0, 2, 0});
+            }
+            SG_TRY(launch_jobs(P, jobs));
         }
         for (int p = 1; p <= ng; ++p) {
             const int lv = L - p;
-            const double* acc = P->wsZ + qoff[0][p - 1];   // Q_{1,p-1} at (1, lv)
-            double* bufs[2] = {P->wsA, P->wsB};
-            int cur = 0;
-            for (int m = 2; m <= p; ++m) {
-                double* dst = bufs[cur];
-                SG_TRY(launch_copy(P, (int64_t)S_in * n1(m) * n2(lv), P->wsZ + qoff[m - 1][p - m], dst));
-                EntryList el;
-                el.ne = 0;
-                for (int s = 0; s < S_in; ++s) el.e[el.ne++] = {acc, P->fx.lev[m].pvals, 1.0, s, s};
-                SG_TRY(launch_gather(P, 0, 2, S_in, n1(m - 1), n2(lv), n1(m), P->fx.lev[m].pcols, el, dst, 1.0));
-                acc = dst;
-                cur ^= 1;
-            }
+            const double* acc = p == 1 ? P->wsZ + qoff[0][0] : hb[p & 1] + offIn[p - 1];
             if (xbox) {
                 XgatParams ep;
                 ep.ne = 0;
@@ -532,44 +534,36 @@ static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in
                     fl.out[0] = P->wsZ + qoff[pp - 1][0];
                     SG_TRY(launch_fanout(P, 0, Wx, S_in, n1(pp), n2(lv), n1(pp), P->fx.lev[pp].cols, X + offIn[pp - 1], fl));
                 }
-                for (int k = 1; k <= pp - 1; ++k) {
-                    const int lf = pp - k + 1, lc = pp - k;
-                    EntryList el;
-                    el.ne = 0;
-                    for (int s = 0; s < S_in; ++s)
-                        el.e[el.ne++] = {P->wsZ + qoff[pp - 1][k - 1], P->fx.lev[lf].rvals, 1.0, s, s};
-                    SG_TRY(launch_gather(P, 0, Wx, S_in, n1(lf), n2(lv), n1(lc), P->fx.lev[lf].rcols, el,
-                                         P->wsZ + qoff[pp - 1][k], 0.0));
+            }
+            // restriction chains in x, batched over sources: stage k maps x-level pp-k+1 -> pp-k
+            for (int k = 1; k <= ng - 1; ++k) {
+                std::vector<Job> jobs;
+                for (int pp = k + 1; pp <= ng; ++pp) {
+                    const int lv = L - pp, lf = pp - k + 1, lc = pp - k;
+                    jobs.push_back({P->wsZ + qoff[pp - 1][k - 1], nullptr, P->wsZ + qoff[pp - 1][k],
+                                    P->fx.lev[lf].rcols, P->fx.lev[lf].rvals, n1(lf), n2(lv), n1(lc), 1.0, S_in, 0, Wx,
+                                    0});
                 }
+                SG_TRY(launch_jobs(P, jobs));
+            }
+            // Horner prolongation in v, batched over targets: at stage q every target p <= ng-q is
+            // lifted from v-level L-ng+q-1 to L-ng+q and gets the source p' = ng-q added (if p' > p)
+            double* hb[2] = {P->wsH, P->wsH + set_size(P, SG_SET_ACTIVE, S_in)};
+            for (int q = 1; q <= ng - 1; ++q) {
+                std::vector<Job> jobs;
+                const int lvn = L - ng + q;
+                for (int p = 1; p <= ng - q; ++p) {
+                    const double* in = q == 1 ? P->wsZ + qoff[ng - 1][ng - p] : hb[(q - 1) & 1] + offIn[p - 1];
+                    const int pp = ng - q;
+                    const double* add = pp > p ? P->wsZ + qoff[pp - 1][pp - p] : nullptr;
+                    jobs.push_back({in, add, hb[q & 1] + offIn[p - 1], P->fv.lev[lvn].pcols, P->fv.lev[lvn].pvals, n1(p),
+                                    n2(lvn - 1), n2(lvn), 1.0, S_in, 1, 2, 0});
+                }
+                SG_TRY(launch_jobs(P, jobs));
             }
             for (int p = 1; p <= ng - 1; ++p) {
                 const int lvt = L - p;
-                // Horner in v: start at source p' = ng (v-level L-ng), end at v-level L-p
-                const double* acc = P->wsZ + qoff[ng - 1][ng - p];
-                int accl = L - ng;
-                double* bufs[2] = {P->wsA, P->wsB};
-                int cur = 0;
-                for (int pp = ng - 1; pp >= p + 1; --pp) {
-                    const int lvn = L - pp;   // = accl + 1
-                    double* dst = bufs[cur];
-                    SG_TRY(launch_copy(P, (int64_t)S_in * n1(p) * n2(lvn), P->wsZ + qoff[pp - 1][pp - p], dst));
-                    EntryList el;
-                    el.ne = 0;
-                    for (int s = 0; s < S_in; ++s) el.e[el.ne++] = {acc, P->fv.lev[lvn].pvals, 1.0, s, s};
-                    SG_TRY(launch_gather(P, 1, 2, S_in, n1(p), n2(accl), n2(lvn), P->fv.lev[lvn].pcols, el, dst, 1.0));
-                    acc = dst;
-                    accl = lvn;
-                    cur ^= 1;
-                }
-                {
-                    // final prolongation to the target v-level
-                    double* dst = bufs[cur];
-                    EntryList el;
-                    el.ne = 0;
-                    for (int s = 0; s < S_in; ++s) el.e[el.ne++] = {acc, P->fv.lev[lvt].pvals, 1.0, s, s};
-                    SG_TRY(launch_gather(P, 1, 2, S_in, n1(p), n2(accl), n2(lvt), P->fv.lev[lvt].pcols, el, dst, 0.0));
-                    acc = dst;
-                }
+                const double* acc = hb[(ng - p) & 1] + offIn[p - 1];   // written at stage q = ng - p
                 if (vbox) {
                     XgatParams ep;
                     ep.ne = 0;
