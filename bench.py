@@ -236,13 +236,21 @@ def main():
     # ---------------------------------------------------------------- roofline
     pk = peaks()
     hbm = pk.get("hbm_gbs", 6650.0)
-    per_launch_ms = kt["ms"] / max(kt["launches"], 1)
-    achieved = (kt["bytes"] / 1e9) / (kt["ms"] / 1e3) if kt["ms"] > 0 else None
-    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": (achieved / hbm) if achieved else None, "traffic": None,
-            "kernel": "strip-operator apply (k_fanout<1,W,*> + k_gather<0,W>) per component grid",
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback 6650 GB/s",
-            "flops_achieved_gflops": (kt["flops"] / 1e9) / (kt["ms"] / 1e3) if kt["ms"] > 0 else None,
+    # fp64 peak from the unit counts of the guides: 148 SMs x 64 FP64 FMA/clk x 2 FLOP x max SM clock
+    sm_max = (pk.get("sm_max_mhz") or 1965.0) / 1e3
+    fp64_peak_tflops = 148 * 64 * 2 * sm_max / 1e3
+    achieved_tf = (kt["flops"] / 1e12) / (kt["ms"] / 1e3) if kt["ms"] > 0 else None
+    achieved_gbs = (kt["bytes"] / 1e9) / (kt["ms"] / 1e3) if kt["ms"] > 0 else None
+    roof = {"bound": "alu", "achieved": achieved_tf, "peak": fp64_peak_tflops, "unit": "TFLOP/s",
+            "frac": (achieved_tf / fp64_peak_tflops) if achieved_tf else None, "traffic": None,
+            "kernel": "strip-operator apply per component grid (k_vfan_st + k_xgat_st, 2-pass stencil kernels)",
+            "peak_source": "derived fp64: 148 SM x 64 FMA/clk x 2 x sm_max_mhz (DESIGN.md sec. 5)",
+            "algorithmic_flops_per_launch": kt["flops"] / max(kt["launches"], 1),
+            "hbm_view": {"achieved_gbs": achieved_gbs, "peak_gbs": hbm,
+                         "frac": (achieved_gbs / hbm) if achieved_gbs else None,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback 6650 GB/s",
+                         "note": "algorithmic bytes = read X + write Y + factor values/patterns"},
+            "traffic_note": "per-launch DRAM bytes from ncu --set full in profiles/ (per grid)",
             "share_of_step": (kt["ms"] / ms) if ms > 0 else None,
             "avg_apply_ms": kt["ms"] / max(st["applies"], 1)}
     clocks = clk.summary()

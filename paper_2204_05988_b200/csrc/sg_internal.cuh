@@ -68,6 +68,7 @@ struct Level {
     std::vector<double*> fst;   // per spec id: stencil format [W][n] (box lattices), nullptr if unused
     std::vector<double*> fcls;  // per spec id: class table [27][W] if translation invariant
     uint8_t* bflag = nullptr;   // 1 for lattice-boundary nodes
+    int64_t nbnd = 0;           // number of boundary nodes
     StencilOff so;              // stencil offsets (box lattices)
 };
 

@@ -39,6 +39,21 @@ static int timed_end(sg_problem* P, cudaEvent_t e0, double bytes, double flops, 
     return SG_OK;
 }
 
+// algorithmic FLOPs of one strip-operator apply on grid g (2 per multiply-add):
+// interior groups on every x-row, boundary-only (face) groups on boundary x-rows only
+static double diag_flops(const sg_problem* P, const Grid& g) {
+    const int S = P->S;
+    const int64_t nb1 = P->fx.lev[g.l1].nbnd;
+    double f = 0.0;
+    for (int o = 0; o < (int)P->vorder.size(); ++o) {
+        const Group& gr = P->vgroups[P->vorder[o]];
+        const double rows = gr.bonly ? (double)nb1 : (double)g.n1;
+        const double ne = (double)gr.comb[g.l1].size();
+        f += 2.0 * rows * g.n2 * (S * P->fv.W + ne * P->fx.W);
+    }
+    return f;
+}
+
 // ------------------------------------------------ diagonal block (one grid)
 // Y = sum_t T_t (x) A_t (x) B_t X, grouped by the v-spec b:
 //   Z_b = (Id x Id x B_b) X           (fanout along v, one read of X per 4 b's)
@@ -90,8 +105,7 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
                 P->dof_applied += S * n;
                 double bytes = 16.0 * S * n + (8.0 * nb + 4.0) * (double)(P->fv.W * g.n2) +
                                (8.0 * ep.ne) * (double)(P->fx.W * g.n1);
-                double flops = 2.0 * S * n * ((double)nb * P->fv.W + (double)ep.ne * P->fx.W);
-                SG_TRY(timed_end(P, e0, bytes, flops, (int)(P->launches - l0)));
+                SG_TRY(timed_end(P, e0, bytes, diag_flops(P, g), (int)(P->launches - l0)));
                 return SG_OK;
             }
             if (rc != SG_ERR_UNSUPPORTED) return rc;
@@ -133,8 +147,7 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
                 P->dof_applied += S * n;
                 double bytes = 16.0 * S * n + (8.0 * nnz_e + 4.0) * (double)(P->fv.W * g.n2) +
                                (8.0 * nxg + 4.0) * (double)(P->fx.W * g.n1);
-                double flops = 2.0 * S * n * ((double)nxg * P->fx.W + (double)nnz_e * P->fv.W);
-                SG_TRY(timed_end(P, e0, bytes, flops, (int)(P->launches - l0)));
+                SG_TRY(timed_end(P, e0, bytes, diag_flops(P, g), (int)(P->launches - l0)));
                 return SG_OK;
             }
             if (rc != SG_ERR_UNSUPPORTED) return rc;
@@ -201,8 +214,7 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
     // algorithmic bytes: read X, write Y, factor matrices (values + pattern)
     double bytes = 16.0 * S * n + (8.0 * nb + 4.0) * (double)(P->fv.W * g.n2) +
                    (8.0 * nnz_x + 4.0) * (double)(P->fx.W * g.n1);
-    double flops = 2.0 * S * n * ((double)nb * P->fv.W + (double)nnz_x * P->fx.W);
-    SG_TRY(timed_end(P, e0, bytes, flops, (int)(P->launches - l0)));
+    SG_TRY(timed_end(P, e0, bytes, diag_flops(P, g), (int)(P->launches - l0)));
     return SG_OK;
 }
 
@@ -226,6 +238,11 @@ int prepare_stencils(sg_problem* P) {
             if (f->kind == SG_MESH_BOX) {
                 k_bflag<<<(int)((L.n + 255) / 256), 256, 0, P->stream>>>(L.n, f->d, L.m, L.lat, L.bflag);
                 P->launches++;
+                {
+                    int64_t inner = 1;
+                    for (int q = 0; q < f->d; ++q) inner *= (L.m - 2);
+                    L.nbnd = L.n - inner;
+                }
                 std::vector<int64_t> offs;
                 for (int S_ = 0; S_ < (1 << f->d); ++S_) {
                     int64_t o = 0, st = 1;
@@ -240,6 +257,7 @@ int prepare_stencils(sg_problem* P) {
                 for (int k = 0; k < 15; ++k) L.so.off[k] = k < (int)offs.size() ? offs[k] : 0;
             } else {
                 SG_CUDA(cudaMemsetAsync(L.bflag, 1, L.n, P->stream));   // no skipping off box lattices
+                L.nbnd = L.n;
             }
         }
     }
