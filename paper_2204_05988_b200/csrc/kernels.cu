@@ -965,3 +965,197 @@ int launch_jobs(sg_problem* P, std::vector<Job>& jobs) {
     return SG_OK;
 }
 }  // namespace sg
+
+namespace sg {
+// =====================================================================
+// x-side gather (pass 2) for 3D box x-lattices with 2x2x2 register bricks.
+// Warp = one brick of 8 target rows (lattice z0 + {0,1}^3) x 32*CPT columns.
+// Every source row of the brick's halo is loaded once and scattered into all
+// targets whose Kuhn stencil contains it (static, fully unrolled); interior
+// bricks of translation-invariant matrices use 15 warp-uniform coefficients.
+// Slot k <-> lattice offset (sorted lexicographic linear offsets, m >= 3):
+// =====================================================================
+__host__ __device__ constexpr int kuhn3_slot(int dx, int dy, int dz) {
+    // returns slot 0..14 or -1 if (dx,dy,dz) is not a Kuhn offset
+    return (dx == -1 && dy == -1 && dz == -1) ? 0 :
+           (dx == 0 && dy == -1 && dz == -1) ? 1 :
+           (dx == -1 && dy == 0 && dz == -1) ? 2 :
+           (dx == 0 && dy == 0 && dz == -1) ? 3 :
+           (dx == -1 && dy == -1 && dz == 0) ? 4 :
+           (dx == 0 && dy == -1 && dz == 0) ? 5 :
+           (dx == -1 && dy == 0 && dz == 0) ? 6 :
+           (dx == 0 && dy == 0 && dz == 0) ? 7 :
+           (dx == 1 && dy == 0 && dz == 0) ? 8 :
+           (dx == 0 && dy == 1 && dz == 0) ? 9 :
+           (dx == 1 && dy == 1 && dz == 0) ? 10 :
+           (dx == 0 && dy == 0 && dz == 1) ? 11 :
+           (dx == 1 && dy == 0 && dz == 1) ? 12 :
+           (dx == 0 && dy == 1 && dz == 1) ? 13 :
+           (dx == 1 && dy == 1 && dz == 1) ? 14 : -1;
+}
+
+template <int SO, int CPT>
+__global__ void __launch_bounds__(256, 1) k_xgat_brick3(int n1, int n2, int m, const uint8_t* __restrict__ xflag,
+                                                        XgatParams ep, double* __restrict__ Y, double beta,
+                                                        int ncoltiles) {
+    constexpr int W = 15;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nbx = (m + 1) / 2;
+    const long long nbricks = (long long)nbx * nbx * nbx;
+    const long long bid = (long long)(blockIdx.x / ncoltiles) * 8 + warp;
+    const int ct = blockIdx.x % ncoltiles;
+    if (bid >= nbricks) return;
+    const int bx = (int)(bid % nbx), by = (int)((bid / nbx) % nbx), bz = (int)(bid / ((long long)nbx * nbx));
+    const int x0 = 2 * bx, y0 = 2 * by, z0 = 2 * bz;
+    int acol[CPT];
+    bool aval[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        acol[c] = ct * 32 * CPT + c * 32 + lane;
+        aval[c] = acol[c] < n2;
+        if (!aval[c]) acol[c] = 0;
+    }
+    // target validity and interior test (class 13 = interior in every axis: 1 + 3 + 9)
+    bool tval[8];
+    bool anyb = false, allint = true;
+    int tcls[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const int x = x0 + (t & 1), y = y0 + ((t >> 1) & 1), z = z0 + (t >> 2);
+        tval[t] = x < m && y < m && z < m;
+        const int cx = x == 0 ? 0 : (x == m - 1 ? 2 : 1), cy = y == 0 ? 0 : (y == m - 1 ? 2 : 1),
+                  cz = z == 0 ? 0 : (z == m - 1 ? 2 : 1);
+        tcls[t] = cx + 3 * cy + 9 * cz;
+        if (tval[t]) {
+            const bool b = xflag[x + (long long)m * (y + (long long)m * z)] != 0;
+            anyb |= b;
+            allint &= (tcls[t] == 13);
+        }
+    }
+    // source rows of the 4x4x4 halo (clamped into the lattice)
+    auto srow = [&](int qx, int qy, int qz) -> long long {
+        int x = x0 + qx, y = y0 + qy, z = z0 + qz;
+        x = x < 0 ? 0 : (x >= m ? m - 1 : x);
+        y = y < 0 ? 0 : (y >= m ? m - 1 : y);
+        z = z < 0 ? 0 : (z >= m ? m - 1 : z);
+        return x + (long long)m * (y + (long long)m * z);
+    };
+    const long long plane = (long long)n1 * n2;
+    double acc[SO][8][CPT];
+#pragma unroll
+    for (int s = 0; s < SO; ++s)
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) acc[s][t][c] = 0.0;
+    for (int e = 0; e < ep.ne; ++e) {
+        const XgatEntry& E = ep.e[e];
+        if (E.bonly && !anyb) continue;
+        const double* Z = E.in + (long long)E.s_in * plane;
+        double tmp[8][CPT];
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) tmp[t][c] = 0.0;
+        if (allint && E.ctab) {
+            double cf[W];
+#pragma unroll
+            for (int k = 0; k < W; ++k) cf[k] = __ldg(E.ctab + 13 * W + k);
+#pragma unroll
+            for (int qz = -1; qz <= 2; ++qz)
+#pragma unroll
+                for (int qy = -1; qy <= 2; ++qy)
+#pragma unroll
+                    for (int qx = -1; qx <= 2; ++qx) {
+                        bool used = false;
+#pragma unroll
+                        for (int t = 0; t < 8; ++t)
+                            used |= kuhn3_slot(qx - (t & 1), qy - ((t >> 1) & 1), qz - (t >> 2)) >= 0;
+                        if (!used) continue;
+                        const double* zr = Z + srow(qx, qy, qz) * n2;
+                        double zv[CPT];
+#pragma unroll
+                        for (int c = 0; c < CPT; ++c) zv[c] = __ldg(zr + acol[c]);
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            const int k = kuhn3_slot(qx - (t & 1), qy - ((t >> 1) & 1), qz - (t >> 2));
+                            if (k >= 0)
+#pragma unroll
+                                for (int c = 0; c < CPT; ++c) tmp[t][c] = fma(cf[k], zv[c], tmp[t][c]);
+                        }
+                    }
+        } else {
+#pragma unroll
+            for (int qz = -1; qz <= 2; ++qz)
+#pragma unroll
+                for (int qy = -1; qy <= 2; ++qy)
+#pragma unroll
+                    for (int qx = -1; qx <= 2; ++qx) {
+                        bool used = false;
+#pragma unroll
+                        for (int t = 0; t < 8; ++t)
+                            used |= kuhn3_slot(qx - (t & 1), qy - ((t >> 1) & 1), qz - (t >> 2)) >= 0;
+                        if (!used) continue;
+                        const double* zr = Z + srow(qx, qy, qz) * n2;
+                        double zv[CPT];
+#pragma unroll
+                        for (int c = 0; c < CPT; ++c) zv[c] = __ldg(zr + acol[c]);
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            const int k = kuhn3_slot(qx - (t & 1), qy - ((t >> 1) & 1), qz - (t >> 2));
+                            if (k >= 0 && tval[t]) {
+                                const int x = x0 + (t & 1), y = y0 + ((t >> 1) & 1), z = z0 + (t >> 2);
+                                const long long it = x + (long long)m * (y + (long long)m * z);
+                                const double cfk = E.ctab ? __ldg(E.ctab + tcls[t] * W + k) : __ldg(E.cst + (long long)k * n1 + it);
+#pragma unroll
+                                for (int c = 0; c < CPT; ++c) tmp[t][c] = fma(cfk, zv[c], tmp[t][c]);
+                            }
+                        }
+                    }
+        }
+#pragma unroll
+        for (int s = 0; s < SO; ++s)
+            if (s == E.s_out)
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+#pragma unroll
+                    for (int c = 0; c < CPT; ++c) acc[s][t][c] = fma(E.scale, tmp[t][c], acc[s][t][c]);
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        if (!tval[t]) continue;
+        const int x = x0 + (t & 1), y = y0 + ((t >> 1) & 1), z = z0 + (t >> 2);
+        const long long it = x + (long long)m * (y + (long long)m * z);
+#pragma unroll
+        for (int s = 0; s < SO; ++s) {
+            double* yr = Y + s * plane + it * n2;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                if (!aval[c]) continue;
+                double* y = yr + acol[c];
+                *y = beta == 0.0 ? acc[s][t][c] : fma(beta, *y, acc[s][t][c]);
+            }
+        }
+    }
+}
+
+int launch_xgat_brick3(sg_problem* P, int S_out, int64_t n1, int64_t n2, int m, const uint8_t* xflag,
+                       const XgatParams& ep, double* Y, double beta) {
+    const int cpt = n2 >= 64 ? 2 : 1;
+    const int64_t ctiles = (n2 + 32 * cpt - 1) / (32 * cpt);
+    const int64_t nbx = (m + 1) / 2;
+    const int64_t nbricks = nbx * nbx * nbx;
+    const int64_t nb = ctiles * ((nbricks + 7) / 8);
+    if (n1 * n2 >= (1LL << 31) || nb >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
+#define XB(SS, CC) k_xgat_brick3<SS, CC><<<(unsigned)nb, 256, 0, P->stream>>>((int)n1, (int)n2, m, xflag, ep, Y, beta, (int)ctiles)
+    if (S_out == 1) {
+        if (cpt == 2) XB(1, 2); else XB(1, 1);
+    } else {
+        if (cpt == 2) XB(2, 2); else XB(2, 1);
+    }
+#undef XB
+    P->launches++;
+    SG_CUDA(cudaGetLastError());
+    return SG_OK;
+}
+}  // namespace sg

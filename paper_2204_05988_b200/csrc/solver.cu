@@ -39,6 +39,14 @@ static int timed_end(sg_problem* P, cudaEvent_t e0, double bytes, double flops, 
     return SG_OK;
 }
 
+// pass-2 dispatcher: 2x2x2 register bricks on 3D box x-lattices, band kernel otherwise
+static int xgather(sg_problem* P, const Grid& g, const XgatParams& ep, double* Y, double beta) {
+    const Level& Lx = P->fx.lev[g.l1];
+    if (P->fx.d == 3 && P->use_brick && Lx.m >= 3)
+        return launch_xgat_brick3(P, P->S, g.n1, g.n2, Lx.m, Lx.bflag, ep, Y, beta);
+    return launch_xgat_st(P, P->fx.d, P->S, g.n1, g.n2, Lx.so, Lx.bflag, ep, Y, beta, Lx.m);
+}
+
 // algorithmic FLOPs of one strip-operator apply on grid g (2 per multiply-add):
 // interior groups on every x-row, boundary-only (face) groups on boundary x-rows only
 static double diag_flops(const sg_problem* P, const Grid& g) {
@@ -184,7 +192,7 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
             const Group& gr = P->vgroups[P->vorder[o]];
             for (const auto& ce : gr.comb[g.l1]) {
                 if (ep.ne == MAX_ENTRIES) {
-                    SG_TRY(launch_xgat_st(P, P->fx.d, S, g.n1, g.n2, Lx.so, Lx.bflag, ep, Y, beta, Lx.m));
+                    SG_TRY(xgather(P, g, ep, Y, beta));
                     beta = 1.0;
                     ep.ne = 0;
                 }
@@ -192,7 +200,7 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
                 nnz_x++;
             }
         }
-        SG_TRY(launch_xgat_st(P, P->fx.d, S, g.n1, g.n2, Lx.so, Lx.bflag, ep, Y, beta, Lx.m));
+        SG_TRY(xgather(P, g, ep, Y, beta));
     } else {
         EntryList el;
         el.ne = 0;
