@@ -64,6 +64,7 @@ extern "C" int sg_create(const sg_config* cfg, void* stream, sg_problem** out) {
     // two-pass kernels on B200 in round-1 measurements: opt-in only
     P->use_fused = getenv("SG_FUSED") != nullptr;
     P->use_graphs = getenv("SG_NO_GRAPHS") == nullptr;
+    P->use_reg = getenv("SG_REG") != nullptr;   // measured slower in round 1: opt-in
     P->use_brick = getenv("SG_BRICK") != nullptr;   // measured 4x slower in round 1: opt-in
     if (cudaStreamCreateWithFlags(&P->gstream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&P->ev_a, cudaEventDisableTiming) != cudaSuccess ||

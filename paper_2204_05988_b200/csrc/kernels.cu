@@ -12,6 +12,7 @@
 // (-1 padded, value 0).  Threads are flattened over (r, c) with c fastest so
 // every warp reads consecutive c (coalesced rows of the block).
 #include <algorithm>
+#include <cstdlib>
 
 #include "sg_internal.cuh"
 
@@ -747,7 +748,8 @@ int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const St
 int launch_xgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
                    const uint8_t* xflag, const XgatParams& ep, double* Y, double beta, int m) {
     constexpr int T = 4;
-    const int cpt = n2 >= 64 ? 2 : 1;
+    static const int cpt_env = getenv("SG_XG_CPT") ? atoi(getenv("SG_XG_CPT")) : 0;
+    const int cpt = cpt_env == 1 ? 1 : (n2 >= 64 ? 2 : 1);
     const int64_t ctiles = (n2 + 32 * cpt - 1) / (32 * cpt);
     const int64_t rgroups = (n1 + 8 * T - 1) / (8 * T);
     const int64_t nb = ctiles * rgroups;
@@ -1154,6 +1156,235 @@ int launch_xgat_brick3(sg_problem* P, int S_out, int64_t n1, int64_t n2, int m, 
         if (cpt == 2) XB(2, 2); else XB(2, 1);
     }
 #undef XB
+    P->launches++;
+    SG_CUDA(cudaGetLastError());
+    return SG_OK;
+}
+}  // namespace sg
+
+namespace sg {
+// =====================================================================
+// Register-coefficient variants (round-1 "reg" kernels).
+// Each multiply-add needs a coefficient and a value; keeping the coefficient in
+// registers and reusing every loaded value for several FMAs is what lifts the
+// FMA/load ratio above 1 on sm_100a (see profiles/README.md sec. 4).
+// =====================================================================
+
+// Pass 1: Z_g[row][a] = sum_k B_g[k][a] X[row][a + off_k].  Thread = (column a,
+// set of VR_G groups); its coefficients stay in registers while it sweeps the
+// rows of its block; the X values of a row are shared by the VR_G groups.
+constexpr int VR_G = 4;
+template <int D>
+__global__ void __launch_bounds__(256, 2) k_vfan_reg(int nrows, int n1, int n2, StencilOff so,
+                                                     const uint8_t* __restrict__ xflag, VfanParams vp,
+                                                     const double* __restrict__ X, int rows_per_block, int nsets) {
+    constexpr int W = stc::Bands<D>::W;
+    const int cols_per_block = 256 / nsets;
+    const int tid = threadIdx.x;
+    const int cl = tid / nsets, set = tid - cl * nsets;
+    if (cl >= cols_per_block) return;
+    const int a = blockIdx.x * cols_per_block + cl;
+    if (a >= n2) return;
+    const int g0 = set * VR_G;
+    double B[VR_G][W];
+    bool gon[VR_G], gbonly[VR_G];
+#pragma unroll
+    for (int q = 0; q < VR_G; ++q) {
+        const int g = g0 + q;
+        gon[q] = g < vp.ng;
+        gbonly[q] = g >= vp.ng_int;
+#pragma unroll
+        for (int k = 0; k < W; ++k) B[q][k] = gon[q] ? __ldg(vp.vst[g] + (long long)k * n2 + a) : 0.0;
+    }
+    int addr[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        int c = a + (int)so.off[k];
+        addr[k] = c < 0 ? 0 : (c >= n2 ? n2 - 1 : c);
+    }
+    const int rb = blockIdx.y * rows_per_block;
+    const int re = min(nrows, rb + rows_per_block);
+    for (int r = rb; r < re; ++r) {
+        const bool bnd = xflag[r % n1] != 0;
+        bool any = false;
+#pragma unroll
+        for (int q = 0; q < VR_G; ++q) any |= gon[q] && (bnd || !gbonly[q]);
+        if (!any) continue;
+        const double* xr = X + (long long)r * n2;
+        double x[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) x[k] = __ldg(xr + addr[k]);
+#pragma unroll
+        for (int q = 0; q < VR_G; ++q) {
+            if (!gon[q] || (gbonly[q] && !bnd)) continue;
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) acc = fma(B[q][k], x[k], acc);
+            vp.out[g0 + q][(long long)r * n2 + a] = acc;
+        }
+    }
+}
+
+int launch_vfan_reg(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, const uint8_t* xflag,
+                    const VfanParams& vp, const double* X) {
+    const int nsets = (vp.ng + VR_G - 1) / VR_G;
+    if (nsets > 8 || (int64_t)S * n1 * n2 >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
+    const int cpb = 256 / nsets;
+    const int64_t nrows = (int64_t)S * n1;
+    const int64_t ctiles = (n2 + cpb - 1) / cpb;
+    int64_t rchunks = std::max<int64_t>(1, (148 * 4 + ctiles - 1) / ctiles);
+    rchunks = std::min<int64_t>(rchunks, std::max<int64_t>(1, nrows / 8));
+    rchunks = std::min<int64_t>(rchunks, 65535);
+    const int rpb = (int)((nrows + rchunks - 1) / rchunks);
+    dim3 grid((unsigned)ctiles, (unsigned)rchunks);
+    if (d == 1) k_vfan_reg<1><<<grid, 256, 0, P->stream>>>((int)nrows, (int)n1, (int)n2, so, xflag, vp, X, rpb, nsets);
+    else if (d == 2) k_vfan_reg<2><<<grid, 256, 0, P->stream>>>((int)nrows, (int)n1, (int)n2, so, xflag, vp, X, rpb, nsets);
+    else k_vfan_reg<3><<<grid, 256, 0, P->stream>>>((int)nrows, (int)n1, (int)n2, so, xflag, vp, X, rpb, nsets);
+    P->launches++;
+    SG_CUDA(cudaGetLastError());
+    return SG_OK;
+}
+
+// Pass 2: Y[s][i][a] = sum_e sum_k C_e[i,k] Z_e[s_in][i + off_k][a].  Block = 8 warps
+// sharing XR_T consecutive target rows x 32 columns; warp w owns the entries
+// e = w, w+8, ...; interior targets of translation-invariant matrices use
+// register coefficients; partial sums are reduced through shared memory.
+constexpr int XR_T = 8;
+template <int D, int SO>
+__global__ void __launch_bounds__(256, 2) k_xgat_reg(int n1, int n2, StencilOff so, int m,
+                                                     const uint8_t* __restrict__ xflag, XgatParams ep,
+                                                     double* __restrict__ Y, double beta, int ncoltiles) {
+    using B = stc::Bands<D>;
+    constexpr int W = B::W;
+    constexpr int MAXL = 3;
+    __shared__ double red[8][SO][XR_T][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int rgroups = (n1 + XR_T - 1) / XR_T;
+    const int ct = blockIdx.x / rgroups, rg = blockIdx.x % rgroups;
+    const int i0 = rg * XR_T;
+    const int a = ct * 32 + lane;
+    const bool aval = a < n2;
+    const int ac = aval ? a : 0;
+    int cls[XR_T];
+    bool anyb = false, allint = true;
+#pragma unroll
+    for (int t = 0; t < XR_T; ++t) {
+        const int it = min(i0 + t, n1 - 1);
+        int z = it, c = 0, mul = 1, interior = 1;
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+            const int zq = z % m;
+            z /= m;
+            const int st = zq == 0 ? 0 : (zq == m - 1 ? 2 : 1);
+            interior &= st == 1;
+            c += mul * st;
+            mul *= 3;
+        }
+        cls[t] = c;
+        if (i0 + t < n1) {
+            anyb |= xflag[it] != 0;
+            allint &= interior != 0;
+        }
+    }
+    int icls = 0;
+    {
+        int mul = 1;
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+            icls += mul;
+            mul *= 3;
+        }
+    }
+    const long long plane = (long long)n1 * n2;
+    double acc[SO][XR_T];
+#pragma unroll
+    for (int s = 0; s < SO; ++s)
+#pragma unroll
+        for (int t = 0; t < XR_T; ++t) acc[s][t] = 0.0;
+    for (int e = warp; e < ep.ne; e += 8) {
+        const XgatEntry& E = ep.e[e];
+        if (E.bonly && !anyb) continue;
+        const double* Z = E.in + (long long)E.s_in * plane;
+        const bool fast = allint && E.ctab != nullptr;
+        double cf[W];
+        if (fast) {
+#pragma unroll
+            for (int k = 0; k < W; ++k) cf[k] = __ldg(E.ctab + icls * W + k);
+        }
+        double tmp[XR_T];
+#pragma unroll
+        for (int t = 0; t < XR_T; ++t) tmp[t] = 0.0;
+#pragma unroll
+        for (int b = 0; b < B::NB; ++b) {
+            const int klo = B::lo(b), len = B::len(b);
+            const int base = i0 + (int)so.off[klo];
+            double z[XR_T + MAXL - 1];
+#pragma unroll
+            for (int q = 0; q < XR_T + MAXL - 1; ++q) {
+                if (q < XR_T + len - 1) {
+                    int r = base + q;
+                    r = r < 0 ? 0 : (r >= n1 ? n1 - 1 : r);
+                    z[q] = __ldg(Z + (long long)r * n2 + ac);
+                }
+            }
+#pragma unroll
+            for (int kk = 0; kk < MAXL; ++kk) {
+                if (kk < len) {
+#pragma unroll
+                    for (int t = 0; t < XR_T; ++t) {
+                        double c;
+                        if (fast) {
+                            c = cf[klo + kk];
+                        } else {
+                            const int it = min(i0 + t, n1 - 1);
+                            c = E.ctab ? __ldg(E.ctab + cls[t] * W + klo + kk)
+                                       : __ldg(E.cst + (long long)(klo + kk) * n1 + it);
+                        }
+                        tmp[t] = fma(c, z[t + kk], tmp[t]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < SO; ++s)
+            if (s == E.s_out)
+#pragma unroll
+                for (int t = 0; t < XR_T; ++t) acc[s][t] = fma(E.scale, tmp[t], acc[s][t]);
+    }
+#pragma unroll
+    for (int s = 0; s < SO; ++s)
+#pragma unroll
+        for (int t = 0; t < XR_T; ++t) red[warp][s][t][lane] = acc[s][t];
+    __syncthreads();
+    // warp w reduces target rows t = w (XR_T = 8 = #warps) for every s
+    {
+        const int t = warp;
+        if (i0 + t < n1 && aval) {
+#pragma unroll
+            for (int s = 0; s < SO; ++s) {
+                double v = 0.0;
+#pragma unroll
+                for (int w = 0; w < 8; ++w) v += red[w][s][t][lane];
+                double* y = Y + s * plane + (long long)(i0 + t) * n2 + a;
+                *y = beta == 0.0 ? v : fma(beta, *y, v);
+            }
+        }
+    }
+}
+
+int launch_xgat_reg(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so, int m,
+                    const uint8_t* xflag, const XgatParams& ep, double* Y, double beta) {
+    const int64_t ctiles = (n2 + 31) / 32;
+    const int64_t rgroups = (n1 + XR_T - 1) / XR_T;
+    const int64_t nb = ctiles * rgroups;
+    if (n1 * n2 >= (1LL << 31) || nb >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
+#define XR(DD, SS) k_xgat_reg<DD, SS><<<(unsigned)nb, 256, 0, P->stream>>>((int)n1, (int)n2, so, m, xflag, ep, Y, beta, (int)ctiles)
+    if (S_out == 1) {
+        if (d == 1) XR(1, 1); else if (d == 2) XR(2, 1); else XR(3, 1);
+    } else {
+        if (d == 1) XR(1, 2); else if (d == 2) XR(2, 2); else XR(3, 2);
+    }
+#undef XR
     P->launches++;
     SG_CUDA(cudaGetLastError());
     return SG_OK;

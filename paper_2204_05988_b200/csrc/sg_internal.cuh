@@ -220,6 +220,7 @@ struct sg_problem {
     bool use_classes = true;
     bool use_graphs = true;
     bool use_brick = true;
+    bool use_reg = true;           // register-coefficient pass kernels
     cudaStream_t gstream = nullptr;   // library stream for captured graphs
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;
     std::vector<sg::GraphEntry> graphs;
@@ -257,6 +258,10 @@ int launch_xgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, cons
                    const uint8_t* xflag, const XgatParams& ep, double* Y, double beta, int m = 0);
 int class_compress(sg_problem* P, const Factor& f, int l, const double* st, double** ctab);
 int launch_jobs(sg_problem* P, std::vector<Job>& jobs);
+int launch_vfan_reg(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, const uint8_t* xflag,
+                    const VfanParams& vp, const double* X);
+int launch_xgat_reg(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so, int m,
+                    const uint8_t* xflag, const XgatParams& ep, double* Y, double beta);
 int launch_xgat_brick3(sg_problem* P, int S_out, int64_t n1, int64_t n2, int m, const uint8_t* xflag,
                        const XgatParams& ep, double* Y, double beta);
 int launch_fused_wx(sg_problem* P, int dv, int dx, int S, int64_t n1, int64_t n2, const StencilOff& sov,

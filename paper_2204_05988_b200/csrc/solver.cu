@@ -44,6 +44,10 @@ static int xgather(sg_problem* P, const Grid& g, const XgatParams& ep, double* Y
     const Level& Lx = P->fx.lev[g.l1];
     if (P->fx.d == 3 && P->use_brick && Lx.m >= 3)
         return launch_xgat_brick3(P, P->S, g.n1, g.n2, Lx.m, Lx.bflag, ep, Y, beta);
+    if (P->use_reg) {
+        int rc = launch_xgat_reg(P, P->fx.d, P->S, g.n1, g.n2, Lx.so, Lx.m, Lx.bflag, ep, Y, beta);
+        if (rc != SG_ERR_UNSUPPORTED) return rc;
+    }
     return launch_xgat_st(P, P->fx.d, P->S, g.n1, g.n2, Lx.so, Lx.bflag, ep, Y, beta, Lx.m);
 }
 
@@ -170,7 +174,9 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
             vp.vst[o] = Lv.fst[P->vgroups[P->vorder[o]].spec];
             vp.out[o] = P->wsZ + (int64_t)o * S * n;
         }
-        SG_TRY(launch_vfan_st(P, P->fv.d, S, g.n1, g.n2, Lv.so, Lx.bflag, vp, X));
+        int rc = P->use_reg ? launch_vfan_reg(P, P->fv.d, S, g.n1, g.n2, Lv.so, Lx.bflag, vp, X) : SG_ERR_UNSUPPORTED;
+        if (rc == SG_ERR_UNSUPPORTED) rc = launch_vfan_st(P, P->fv.d, S, g.n1, g.n2, Lv.so, Lx.bflag, vp, X);
+        SG_TRY(rc);
     } else {
         for (int b0 = 0; b0 < nb; b0 += MAX_FANOUT) {
             FanoutList fl;

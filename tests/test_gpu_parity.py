@@ -249,7 +249,7 @@ def test_zero_rhs_gives_zero():
     assert it == 1 and float(u.abs().max()) == 0.0
 
 
-@pytest.mark.parametrize("env", ["SG_FUSED", "SG_FORCE_XFIRST", "SG_BRICK"])
+@pytest.mark.parametrize("env", ["SG_FUSED", "SG_FORCE_XFIRST", "SG_BRICK", "SG_REG"])
 @pytest.mark.parametrize("name", CONFIG_ORDER)
 def test_apply_strip_operator_kernel_paths(name, env, monkeypatch):
     """Same parity on every kernel path at test sizes: the opt-in fused whole-x
