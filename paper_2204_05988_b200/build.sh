@@ -6,11 +6,13 @@ cd "$HERE/csrc"
 NVCC=${NVCC:-/usr/local/cuda/bin/nvcc}
 FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr $*"
 OBJS=""
-for f in mesh assemble kernels setup solver api; do
+PIDS=""
+for f in mesh assemble kernels xfanin xfanin_tma setup solver api; do
   $NVCC $FLAGS -dc -o "$f.o" "$f.cu" &
+  PIDS="$PIDS $!"
   OBJS="$OBJS $f.o"
 done
-wait
+for p in $PIDS; do wait $p; done   # set -e: any failed compile aborts the build
 $NVCC -gencode arch=compute_100a,code=sm_100a -shared -o "$HERE/libsg.so" $OBJS -lcudart
 rm -f $OBJS
 echo "built $HERE/libsg.so"

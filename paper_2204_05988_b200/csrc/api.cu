@@ -66,6 +66,10 @@ extern "C" int sg_create(const sg_config* cfg, void* stream, sg_problem** out) {
     P->use_graphs = getenv("SG_NO_GRAPHS") == nullptr;
     P->use_reg = getenv("SG_REG") != nullptr;   // measured slower in round 1: opt-in
     P->use_brick = getenv("SG_BRICK") != nullptr;   // measured 4x slower in round 1: opt-in
+    P->use_xfanin = getenv("SG_OLD_XG") == nullptr;
+    P->use_xfi_tma = getenv("SG_NO_TMA") == nullptr;
+    P->xfi_cpt = getenv("SG_XFI_CPT") ? atoi(getenv("SG_XFI_CPT")) : 1;
+    P->xfi_seg = getenv("SG_XFI_SEG") ? atoi(getenv("SG_XFI_SEG")) : 0;
     if (cudaStreamCreateWithFlags(&P->gstream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&P->ev_a, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&P->ev_b, cudaEventDisableTiming) != cudaSuccess) {
@@ -160,8 +164,9 @@ extern "C" int sg_assemble_factors(sg_problem* P) {
     SG_TRY(prepare_stencils(P));
     // workspaces
     int64_t maxg = 0;
-    for (auto& g : P->active) maxg = std::max(maxg, g.n1 * g.n2);
-    for (auto& g : P->coarse) maxg = std::max(maxg, g.n1 * g.n2);
+    // (even row pitch of the pass-2 intermediates, TMA strides are multiples of 16 bytes)
+    for (auto& g : P->active) maxg = std::max(maxg, g.n1 * (g.n2 + (g.n2 & 1)));
+    for (auto& g : P->coarse) maxg = std::max(maxg, g.n1 * (g.n2 + (g.n2 & 1)));
     const int ng = (int)P->active.size();
     int64_t chain = 0, chain_up = 0;
     for (int pp = 1; pp <= ng; ++pp)

@@ -262,7 +262,8 @@ constexpr int VF_RL = 8;    // row lanes per block
 template <int D, int R>
 __global__ void __launch_bounds__(VF_TC * VF_RL, 2) k_vfan_st(int64_t nrows, int64_t n1, int64_t n2, StencilOff so,
                                                               const uint8_t* __restrict__ xflag, VfanParams vp,
-                                                              const double* __restrict__ X, int64_t rows_per_block) {
+                                                              const double* __restrict__ X, int64_t rows_per_block,
+                                                              int64_t opitch) {
     constexpr int W = stc::Bands<D>::W;
     extern __shared__ double sm[];
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(VF_TC * VF_RL, 2) k_vfan_st(int64_t nrows, int
             double* o = vp.out[g];
 #pragma unroll
             for (int r = 0; r < R; ++r)
-                if (r0 + r < re && aval) o[(r0 + r) * n2 + a] = acc[r];
+                if (r0 + r < re && aval) o[(r0 + r) * opitch + a] = acc[r];
         }
     }
 }
@@ -719,7 +720,8 @@ int class_compress(sg_problem* P, const Factor& f, int l, const double* st, doub
 }
 
 int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, const uint8_t* xflag,
-                   const VfanParams& vp, const double* X) {
+                   const VfanParams& vp, const double* X, int64_t opitch) {
+    if (opitch <= 0) opitch = n2;
     const int W = (1 << (d + 1)) - 1;
     const int64_t nrows = (int64_t)S * n1;
     const int64_t ctiles = (n2 + VF_TC - 1) / VF_TC;
@@ -732,13 +734,13 @@ int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const St
     dim3 grid((unsigned)ctiles, (unsigned)rchunks), block(VF_TC, VF_RL);
     if (d == 1) {
         cudaFuncSetAttribute(k_vfan_st<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_vfan_st<1, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb);
+        k_vfan_st<1, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch);
     } else if (d == 2) {
         cudaFuncSetAttribute(k_vfan_st<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_vfan_st<2, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb);
+        k_vfan_st<2, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch);
     } else {
         cudaFuncSetAttribute(k_vfan_st<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_vfan_st<3, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb);
+        k_vfan_st<3, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch);
     }
     P->launches++;
     SG_CUDA(cudaGetLastError());

@@ -224,6 +224,11 @@ struct sg_problem {
     cudaStream_t gstream = nullptr;   // library stream for captured graphs
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;
     std::vector<sg::GraphEntry> graphs;
+    bool use_xfanin = true;        // line-swept x fan-in pass 2 (SG_OLD_XG disables)
+    int xfi_cpt = 1, xfi_seg = 0;
+    bool use_xfi_tma = true;       // TMA-pipelined pass 2 (SG_NO_TMA disables)  // SG_XFI_CPT (columns per lane), SG_XFI_SEG (sweep segment length, 0 auto)
+    std::vector<double*> xfi_tab;  // per x-level: class table [3^d][groups][W] of the combined x matrices
+    std::vector<std::vector<double>> xfi_cint;   // per x-level: interior-class coefficients [12][15]
     bool use_fused = false;        // opt-in fused whole-x kernel (SG_FUSED)
     int xfirst_mode = 0;           // 0 auto (n1 > n2), 1 never, 2 always (tests)
     int* egrp_dev = nullptr;       // group index of every diag gather entry (fused kernels)
@@ -253,7 +258,7 @@ int launch_zero(sg_problem* P, int64_t n, double* y);
 int launch_ell_to_stencil(sg_problem* P, int64_t n, int W, const int32_t* cols, const double* vals,
                           const StencilOff& so, double* out);
 int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, const uint8_t* xflag,
-                   const VfanParams& vp, const double* X);
+                   const VfanParams& vp, const double* X, int64_t opitch = 0);
 int launch_xgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
                    const uint8_t* xflag, const XgatParams& ep, double* Y, double beta, int m = 0);
 int class_compress(sg_problem* P, const Factor& f, int l, const double* st, double** ctab);
@@ -271,6 +276,13 @@ int launch_vgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, cons
                    const XgatParams& ep, double* Y, double beta, const uint8_t* xflag = nullptr);
 int launch_xfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, int m,
                    const uint8_t* xflag, const XfanParams& fp, const double* X);
+// xfanin.cu
+int prepare_xfanin(sg_problem* P);
+int launch_xfanin(sg_problem* P, int l1, int64_t n1, int64_t n2, const double* Z, int64_t gstride, double* Y,
+                  double beta);
+// xfanin_tma.cu
+int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pitch, const double* Z,
+                      int64_t gstride, double* Y);
 // solver.cu
 int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y);
 int apply_cross(sg_problem* P, const std::vector<Term>* terms_override, const double* Tb, int S_out, int S_in,

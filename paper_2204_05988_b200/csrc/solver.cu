@@ -66,6 +66,11 @@ static double diag_flops(const sg_problem* P, const Grid& g) {
     return f;
 }
 
+static bool l_has_xfi(const sg_problem* P, int l1) {
+    return l1 < (int)P->xfi_tab.size() && P->xfi_tab[l1] != nullptr &&
+           ((P->fx.d == 3 && P->ng_int == 10) || (P->fx.d == 2 && P->ng_int == 6)) && P->fx.lev[l1].m >= 3;
+}
+
 // ------------------------------------------------ diagonal block (one grid)
 // Y = sum_t T_t (x) A_t (x) B_t X, grouped by the v-spec b:
 //   Z_b = (Id x Id x B_b) X           (fanout along v, one read of X per 4 b's)
@@ -166,16 +171,25 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
         }
     }
     // ---- pass 1: Z_b = (Id x Id x B_b) X for every v-group b (interior groups first)
+    // (TMA pass 2 reads the intermediates with an even row pitch)
+    const bool tma2 = vbox && xbox && P->use_xfanin && P->use_xfi_tma && !P->use_brick && !P->use_reg && S == 1 &&
+                      l_has_xfi(P, g.l1);
+    const int64_t pitch = tma2 ? g.n2 + (g.n2 & 1) : g.n2;
+    const int64_t gstr = (int64_t)S * g.n1 * pitch;
+    if ((size_t)nb * gstr > P->wsZ_n) {
+        set_error("apply_diag: workspace too small");
+        return SG_ERR_STATE;
+    }
     if (vbox) {
         VfanParams vp;
         vp.ng = nb;
         vp.ng_int = P->ng_int;
         for (int o = 0; o < nb; ++o) {
             vp.vst[o] = Lv.fst[P->vgroups[P->vorder[o]].spec];
-            vp.out[o] = P->wsZ + (int64_t)o * S * n;
+            vp.out[o] = P->wsZ + (int64_t)o * gstr;
         }
         int rc = P->use_reg ? launch_vfan_reg(P, P->fv.d, S, g.n1, g.n2, Lv.so, Lx.bflag, vp, X) : SG_ERR_UNSUPPORTED;
-        if (rc == SG_ERR_UNSUPPORTED) rc = launch_vfan_st(P, P->fv.d, S, g.n1, g.n2, Lv.so, Lx.bflag, vp, X);
+        if (rc == SG_ERR_UNSUPPORTED) rc = launch_vfan_st(P, P->fv.d, S, g.n1, g.n2, Lv.so, Lx.bflag, vp, X, pitch);
         SG_TRY(rc);
     } else {
         for (int b0 = 0; b0 < nb; b0 += MAX_FANOUT) {
@@ -191,7 +205,22 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
     // ---- pass 2: Y = sum_b sum_{s,s'} (e_s e_s'^T (x) C_b^{ss'} (x) Id) Z_b
     int64_t nnz_x = 0;
     double beta = 0.0;
-    if (xbox) {
+    int rcx = SG_ERR_UNSUPPORTED;
+    if (tma2) {
+        rcx = launch_xfanin_tma(P, g.l1, g.n1, g.n2, pitch, P->wsZ, gstr, Y);
+        if (rcx != SG_OK && rcx != SG_ERR_UNSUPPORTED) return rcx;
+        if (rcx == SG_ERR_UNSUPPORTED && pitch != g.n2) {
+            set_error("apply_diag: TMA pass 2 rejected a padded layout");
+            return SG_ERR_STATE;
+        }
+    }
+    if (rcx != SG_OK && xbox && P->use_xfanin && !P->use_brick && !P->use_reg) {
+        rcx = launch_xfanin(P, g.l1, g.n1, g.n2, P->wsZ, (int64_t)S * n, Y, 0.0);
+        if (rcx != SG_OK && rcx != SG_ERR_UNSUPPORTED) return rcx;
+    }
+    if (rcx == SG_OK) {
+        for (int o = 0; o < nb; ++o) nnz_x += (int64_t)P->vgroups[P->vorder[o]].comb[g.l1].size();
+    } else if (xbox) {
         XgatParams ep;
         ep.ne = 0;
         for (int o = 0; o < nb; ++o) {
@@ -357,6 +386,7 @@ int prepare_stencils(sg_problem* P) {
         SG_CUDA(cudaMalloc(&P->egrp_dev, sizeof(int) * MAX_ENTRIES));
         SG_CUDA(cudaMemcpy(P->egrp_dev, eg.data(), sizeof(int) * P->egrp_n, cudaMemcpyHostToDevice));
     }
+    SG_TRY(prepare_xfanin(P));
     SG_CUDA(cudaStreamSynchronize(P->stream));
     return SG_OK;
 }

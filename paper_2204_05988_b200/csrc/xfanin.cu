@@ -1,0 +1,339 @@
+// Pass 2 of the strip-operator apply on box x-lattices ("x fan-in", line-swept):
+//
+//   Y[i][a] = beta*Y[i][a] + sum_g sum_k C_g^{cls(i)}[k] Z_g[i + off_k][a]
+//
+// (PAPER.md l.462-477 / l.516-532: the x-factor of every Kronecker term, applied
+// after the v-factor; C_g = sum_{t in g} T_t A_t is the time-combined x matrix of
+// v-group g, translation invariant on the lattice up to the boundary class of
+// the row, cls = per axis {low face, interior, high face}).
+//
+// Work decomposition.  An x-lattice "line" is the set of rows with fixed
+// (i1, i2) (axis 0 fastest).  One warp owns a block of target lines (2x2 lines
+// for d = 3, 4 lines for d = 2) and 32*CPT v-columns (lane = column, coalesced),
+// and sweeps the line position i0 = t from 0 to m-1.  At every t it loads, for
+// every group g, the source points (line s, t) of the 14 (d = 3) / 6 (d = 2)
+// lines that neighbour the block exactly once and scatters them into a rolling
+// window of accumulators for the target positions t-1, t, t+1 (registers).
+// Each Z value is therefore read once per line block (3.5 / 1.5 loads per
+// output and group instead of W), and the Kuhn stencil becomes 60 / 28
+// register FMAs per source step.
+//
+// Coefficients.  Away from the lattice boundary (all targets interior) the
+// class is the interior one and the coefficients are compile-time indexed
+// kernel parameters (constant-bank operands of DFMA, no loads); near the
+// boundary they are read from the class table tab[cls][g][k] with warp-uniform
+// addresses (broadcast), and the boundary-only (face) groups are included.
+#include <cstdlib>
+#include <cstring>
+
+#include "sg_internal.cuh"
+
+namespace sg {
+namespace xfi {
+
+// Kuhn offsets (d0, d1, d2) in the sorted order of StencilOff (lexicographic
+// value d0 + m d1 + m^2 d2, m >= 3)
+__host__ __device__ constexpr int d0_3(int k) {
+    return k == 0 ? -1 : k == 1 ? 0 : k == 2 ? -1 : k == 3 ? 0 : k == 4 ? -1 : k == 5 ? 0 : k == 6 ? -1 : k == 7 ? 0
+         : k == 8 ? 1 : k == 9 ? 0 : k == 10 ? 1 : k == 11 ? 0 : k == 12 ? 1 : k == 13 ? 0 : 1;
+}
+__host__ __device__ constexpr int d1_3(int k) {
+    return k == 0 ? -1 : k == 1 ? -1 : k == 2 ? 0 : k == 3 ? 0 : k == 4 ? -1 : k == 5 ? -1 : k == 6 ? 0 : k == 7 ? 0
+         : k == 8 ? 0 : k == 9 ? 1 : k == 10 ? 1 : k == 11 ? 0 : k == 12 ? 0 : k == 13 ? 1 : 1;
+}
+__host__ __device__ constexpr int d2_3(int k) { return k < 4 ? -1 : (k < 11 ? 0 : 1); }
+__host__ __device__ constexpr int d0_2(int k) {
+    return k == 0 ? -1 : k == 1 ? 0 : k == 2 ? -1 : k == 3 ? 0 : k == 4 ? 1 : k == 5 ? 0 : 1;
+}
+__host__ __device__ constexpr int d1_2(int k) { return k < 2 ? -1 : (k < 5 ? 0 : 1); }
+
+template <int D> struct Geo;
+template <> struct Geo<3> {
+    static constexpr int W = 15, NT = 4, NE1 = 4, NE2 = 4;   // 2x2 target lines, sources e in [-1,2]^2
+    static constexpr int B1 = 2, B2 = 2;
+    __host__ __device__ static constexpr int u1(int u) { return u & 1; }
+    __host__ __device__ static constexpr int u2(int u) { return u >> 1; }
+    __host__ __device__ static constexpr int d0(int k) { return d0_3(k); }
+    __host__ __device__ static constexpr int d1(int k) { return d1_3(k); }
+    __host__ __device__ static constexpr int d2(int k) { return d2_3(k); }
+};
+template <> struct Geo<2> {
+    static constexpr int W = 7, NT = 4, NE1 = 6, NE2 = 1;    // 4 target lines, sources e1 in [-1,4]
+    static constexpr int B1 = 4, B2 = 1;
+    __host__ __device__ static constexpr int u1(int u) { return u; }
+    __host__ __device__ static constexpr int u2(int) { return 0; }
+    __host__ __device__ static constexpr int d0(int k) { return d0_2(k); }
+    __host__ __device__ static constexpr int d1(int k) { return d1_2(k); }
+    __host__ __device__ static constexpr int d2(int) { return 0; }
+};
+
+template <int D>
+__host__ __device__ constexpr bool pair_ok(int s, int u, int k) {
+    using G = Geo<D>;
+    return (s % G::NE1) - 1 == G::u1(u) + G::d1(k) && (s / G::NE1) - (D == 3 ? 1 : 0) == G::u2(u) + G::d2(k);
+}
+template <int D>
+__host__ __device__ constexpr bool src_used(int s) {
+    for (int u = 0; u < Geo<D>::NT; ++u)
+        for (int k = 0; k < Geo<D>::W; ++k)
+            if (pair_ok<D>(s, u, k)) return true;
+    return false;
+}
+
+}  // namespace xfi
+
+constexpr int XFI_MAXG = 12;
+struct XfiCoef {
+    double c[XFI_MAXG][15];   // interior-class coefficients of the interior groups
+};
+
+template <int D, int NGI, int CPT>
+__global__ void __launch_bounds__(256, CPT == 1 ? 2 : 1)
+    k_xfanin(const double* __restrict__ Z, long long gstride, int nga, int n2, int m, int nlb1, int nlb, int nseg,
+             int seglen, int nsub, int ntask, const double* __restrict__ tab, const __grid_constant__ XfiCoef cint,
+             double* __restrict__ Y, double beta) {
+    using G = xfi::Geo<D>;
+    constexpr int W = G::W, NT = G::NT, NS = G::NE1 * G::NE2;
+    const int lane = threadIdx.x & 31;
+    // tasks = (line block, segment of the line sweep, column tile); a warp runs nsub
+    // tasks side by side when the v factor has fewer than 32 columns
+    int sub = 0, cl = lane;
+    if (nsub > 1) {
+        sub = lane / n2;
+        cl = lane - sub * n2;
+        if (sub >= nsub) return;
+    }
+    const int task = (blockIdx.x * 8 + (threadIdx.x >> 5)) * nsub + sub;
+    if (task >= ntask) return;
+    const int lb = task % nlb, rest = task / nlb;
+    const int seg = rest % nseg, ct = rest / nseg;
+    const int t0 = seg * seglen, t1 = min(m, t0 + seglen);
+    // target line block origin
+    const int b1 = (lb % nlb1) * G::B1, b2 = (lb / nlb1) * G::B2;
+    int col[CPT];
+    bool cval[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        col[c] = ct * 32 * CPT + c * 32 + cl;
+        cval[c] = col[c] < n2;
+        if (!cval[c]) col[c] = n2 - 1;
+    }
+    // source line bases (element index of (t = 0, line s, column col[0])); clamped lines
+    // only ever meet zero coefficients (absent neighbours of boundary rows)
+    int sbase[NS];
+    bool lines_interior = true;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        int e1 = b1 + (s % G::NE1) - 1;
+        int e2 = D == 3 ? b2 + (s / G::NE1) - 1 : 0;
+        e1 = e1 < 0 ? 0 : (e1 >= m ? m - 1 : e1);
+        e2 = e2 < 0 ? 0 : (e2 >= m ? m - 1 : e2);
+        const int line = D == 3 ? e1 + m * e2 : e1;
+        sbase[s] = line * m * n2 + col[0];
+    }
+    // target lines
+    int tline[NT];
+    bool tval[NT];
+    int tcls12[NT];   // class contribution of axes 1, 2
+#pragma unroll
+    for (int u = 0; u < NT; ++u) {
+        const int z1 = b1 + G::u1(u), z2 = D == 3 ? b2 + G::u2(u) : 0;
+        tval[u] = z1 < m && z2 < m;
+        tline[u] = D == 3 ? z1 + m * z2 : z1;
+        const int c1 = z1 == 0 ? 0 : (z1 >= m - 1 ? 2 : 1);
+        const int c2 = z2 == 0 ? 0 : (z2 >= m - 1 ? 2 : 1);
+        tcls12[u] = 3 * c1 + (D == 3 ? 9 * c2 : 0);
+        lines_interior &= tval[u] && c1 == 1 && (D == 2 || c2 == 1);
+    }
+    double acc[NT][3][CPT];
+#pragma unroll
+    for (int u = 0; u < NT; ++u)
+#pragma unroll
+        for (int w = 0; w < 3; ++w)
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) acc[u][w][c] = 0.0;
+
+    auto flush = [&](int p) {   // target position p complete in window slot 0
+#pragma unroll
+        for (int u = 0; u < NT; ++u) {
+            if (!tval[u]) continue;
+            double* yr = Y + ((long long)p + (long long)m * tline[u]) * n2;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                if (!cval[c]) continue;
+                double* y = yr + col[c];
+                *y = beta == 0.0 ? acc[u][0][c] : fma(beta, *y, acc[u][0][c]);
+            }
+        }
+    };
+
+    const int ts = max(t0 - 1, 0), te = min(t1, m - 1);   // sources of the targets [t0, t1)
+    for (int t = ts; t <= te; ++t) {
+        const long long toff = (long long)t * n2;
+        if (lines_interior && t >= 2 && t <= m - 3) {
+            // ---- interior: constant coefficients from the kernel parameters
+#pragma unroll
+            for (int g = 0; g < NGI; ++g) {
+                const double* Zg = Z + g * gstride + toff;
+                double src[NS][CPT];
+#pragma unroll
+                for (int s = 0; s < NS; ++s)
+                    if (xfi::src_used<D>(s))
+#pragma unroll
+                        for (int c = 0; c < CPT; ++c) src[s][c] = __ldg(Zg + sbase[s] + 32 * c);
+#pragma unroll
+                for (int s = 0; s < NS; ++s)
+#pragma unroll
+                    for (int u = 0; u < NT; ++u)
+#pragma unroll
+                        for (int k = 0; k < W; ++k)
+                            if (xfi::pair_ok<D>(s, u, k)) {
+                                const double cf = cint.c[g][k];
+                                const int slot = 1 - G::d0(k);
+#pragma unroll
+                                for (int c = 0; c < CPT; ++c) acc[u][slot][c] = fma(cf, src[s][c], acc[u][slot][c]);
+                            }
+            }
+        } else {
+            // ---- boundary: class-table coefficients, all groups (incl. face groups)
+            int cb[NT][3];
+#pragma unroll
+            for (int u = 0; u < NT; ++u)
+#pragma unroll
+                for (int w = 0; w < 3; ++w) {
+                    const int p = t + w - 1;
+                    const int c0 = p <= 0 ? 0 : (p >= m - 1 ? 2 : 1);
+                    cb[u][w] = (c0 + tcls12[u]) * nga * W;
+                }
+            for (int g = 0; g < nga; ++g) {
+                const double* Zg = Z + g * gstride + toff;
+                const double* tg = tab + g * W;
+                double src[NS][CPT];
+#pragma unroll
+                for (int s = 0; s < NS; ++s)
+                    if (xfi::src_used<D>(s))
+#pragma unroll
+                        for (int c = 0; c < CPT; ++c) src[s][c] = __ldg(Zg + sbase[s] + 32 * c);
+#pragma unroll
+                for (int s = 0; s < NS; ++s)
+#pragma unroll
+                    for (int u = 0; u < NT; ++u)
+#pragma unroll
+                        for (int k = 0; k < W; ++k)
+                            if (xfi::pair_ok<D>(s, u, k)) {
+                                const int slot = 1 - G::d0(k);
+                                const double cf = __ldg(tg + cb[u][slot] + k);
+#pragma unroll
+                                for (int c = 0; c < CPT; ++c) acc[u][slot][c] = fma(cf, src[s][c], acc[u][slot][c]);
+                            }
+            }
+        }
+        if (t - 1 >= t0) flush(t - 1);
+#pragma unroll
+        for (int u = 0; u < NT; ++u)
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                acc[u][0][c] = acc[u][1][c];
+                acc[u][1][c] = acc[u][2][c];
+                acc[u][2][c] = 0.0;
+            }
+    }
+    if (t1 == m) flush(m - 1);
+}
+
+// host: class tables of the combined x matrices of every v-group (vorder) per x-level
+int prepare_xfanin(sg_problem* P) {
+    P->xfi_tab.assign(P->F + 1, nullptr);
+    P->xfi_cint.assign(P->F + 1, {});
+    if (P->fx.kind != SG_MESH_BOX || P->S != 1 || P->fx.d < 2 || !P->use_classes) return SG_OK;
+    const int nga = (int)P->vorder.size();
+    if (P->ng_int > XFI_MAXG) return SG_OK;
+    const int d = P->fx.d, W = P->fx.W;
+    int ncls = 1, icls = 0, mul = 1;
+    for (int q = 0; q < d; ++q) {
+        icls += mul;
+        mul *= 3;
+        ncls *= 3;
+    }
+    for (int l = 1; l <= P->F; ++l) {
+        std::vector<double> h((size_t)ncls * nga * W, 0.0);
+        bool ok = true;
+        for (int o = 0; o < nga && ok; ++o) {
+            const Group& gr = P->vgroups[P->vorder[o]];
+            if (gr.comb[l].size() != 1 || !gr.comb[l][0].ctab) {
+                ok = false;
+                break;
+            }
+            std::vector<double> t27(27 * W);
+            SG_CUDA(cudaMemcpy(t27.data(), gr.comb[l][0].ctab, sizeof(double) * 27 * W, cudaMemcpyDeviceToHost));
+            for (int c = 0; c < ncls; ++c)
+                for (int k = 0; k < W; ++k) h[((size_t)c * nga + o) * W + k] = t27[c * W + k];
+        }
+        if (!ok) continue;
+        double* dt;
+        SG_CUDA(cudaMalloc(&dt, sizeof(double) * h.size()));
+        SG_CUDA(cudaMemcpy(dt, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+        P->xfi_tab[l] = dt;
+        std::vector<double> ci((size_t)XFI_MAXG * 15, 0.0);
+        for (int o = 0; o < P->ng_int; ++o)
+            for (int k = 0; k < W; ++k) ci[o * 15 + k] = h[((size_t)icls * nga + o) * W + k];
+        P->xfi_cint[l] = ci;
+    }
+    return SG_OK;
+}
+
+// Y = beta*Y + sum_g C_g Z_g over the v-groups of the diagonal apply of grid g;
+// SG_ERR_UNSUPPORTED when the line-swept kernel does not cover this shape.
+int launch_xfanin(sg_problem* P, int l1, int64_t n1, int64_t n2, const double* Z, int64_t gstride, double* Y,
+                  double beta) {
+    if (l1 >= (int)P->xfi_tab.size() || !P->xfi_tab[l1]) return SG_ERR_UNSUPPORTED;
+    const int d = P->fx.d, m = P->fx.lev[l1].m;
+    const int nga = (int)P->vorder.size(), ngi = P->ng_int;
+    if (m < 3 || n1 * n2 >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
+    const int cpt = (P->xfi_cpt == 2 && n2 >= 64) ? 2 : 1;
+    const int nct = (int)((n2 + 32 * cpt - 1) / (32 * cpt));
+    const int nsub = n2 <= 16 ? (int)(32 / n2) : 1;
+    int nlb1, nlb;
+    if (d == 3) {
+        nlb1 = (m + 1) / 2;
+        nlb = nlb1 * nlb1;
+    } else {
+        nlb1 = (m + 3) / 4;
+        nlb = nlb1;
+    }
+    // split the line sweep into segments until the machine has >= 16 warps per SM of work
+    const int seg_env = P->xfi_seg;
+    int seglen = m;
+    if (seg_env > 0) {
+        seglen = seg_env;
+    } else {
+        while (seglen > 16 && (long long)nlb * nct * ((m + seglen - 1) / seglen) < 148LL * 16 * nsub)
+            seglen = (seglen + 1) / 2;
+    }
+    const int nseg = (m + seglen - 1) / seglen;
+    const long long ntask = (long long)nlb * nseg * nct;
+    const long long warps = (ntask + nsub - 1) / nsub;
+    const long long blocks = (warps + 7) / 8;
+    if (ntask >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
+    XfiCoef ci;
+    std::memcpy(ci.c, P->xfi_cint[l1].data(), sizeof(ci.c));
+    const double* tab = P->xfi_tab[l1];
+#define XFI(DD, NG, CC)                                                                                           \
+    k_xfanin<DD, NG, CC><<<(unsigned)blocks, 256, 0, P->stream>>>(Z, (long long)gstride, nga, (int)n2, m, nlb1, nlb, \
+                                                                  nseg, seglen, nsub, (int)ntask, tab, ci, Y, beta)
+#define XFI_C(DD, NG) do { if (cpt == 2) XFI(DD, NG, 2); else XFI(DD, NG, 1); } while (0)
+    if (d == 3 && ngi == 10) XFI_C(3, 10);
+    else if (d == 2 && ngi == 6) XFI_C(2, 6);
+    else if (d == 3 && ngi == 6) XFI_C(3, 6);
+    else if (d == 2 && ngi == 10) XFI_C(2, 10);
+    else if (d == 2 && ngi == 3) XFI_C(2, 3);
+    else if (d == 3 && ngi == 4) XFI_C(3, 4);
+    else return SG_ERR_UNSUPPORTED;
+#undef XFI_C
+#undef XFI
+    P->launches++;
+    SG_CUDA(cudaGetLastError());
+    return SG_OK;
+}
+
+}  // namespace sg

@@ -1,0 +1,419 @@
+// Pass 2 of the strip-operator apply on box x-lattices, TMA-pipelined version
+// of the line-swept x fan-in (xfanin.cu has the register-only variant and the
+// derivation):
+//
+//   Y[i][a] = sum_g sum_k C_g^{cls(i)}[k] Z_g[i + off_k][a]
+//
+// A CTA owns a tile of target x-lines (WL1 x WL2 warp blocks of 2x2 lines for
+// d = 3, WL1 blocks of 4 lines for d = 2) and 32*WC v-columns, and sweeps the
+// line position t.  For every (t, g) one elected producer thread issues ONE
+// cp.async.bulk.tensor load of the box
+//     Z_g[t][halo lines of the tile][32*WC columns]
+// into a ring of shared-memory stages (mbarrier complete_tx); lattice lines
+// outside the domain and columns >= n2 arrive as zeros (TMA out-of-bounds fill),
+// which only ever meet zero coefficients.  The consumer warps scatter the stage
+// into a rolling register window of targets t-1, t, t+1 exactly as the register
+// kernel does (interior coefficients as compile-time kernel parameters, class
+// tables near the boundary), then release the stage.  Z uses an even row pitch
+// (TMA strides must be multiples of 16 bytes).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <cstring>
+
+#include "sg_internal.cuh"
+
+namespace sg {
+namespace xft {
+// Kuhn offsets in StencilOff order (same tables as xfanin.cu)
+__host__ __device__ constexpr int d0_3(int k) {
+    return k == 0 ? -1 : k == 1 ? 0 : k == 2 ? -1 : k == 3 ? 0 : k == 4 ? -1 : k == 5 ? 0 : k == 6 ? -1 : k == 7 ? 0
+         : k == 8 ? 1 : k == 9 ? 0 : k == 10 ? 1 : k == 11 ? 0 : k == 12 ? 1 : k == 13 ? 0 : 1;
+}
+__host__ __device__ constexpr int d1_3(int k) {
+    return k == 0 ? -1 : k == 1 ? -1 : k == 2 ? 0 : k == 3 ? 0 : k == 4 ? -1 : k == 5 ? -1 : k == 6 ? 0 : k == 7 ? 0
+         : k == 8 ? 0 : k == 9 ? 1 : k == 10 ? 1 : k == 11 ? 0 : k == 12 ? 0 : k == 13 ? 1 : 1;
+}
+__host__ __device__ constexpr int d2_3(int k) { return k < 4 ? -1 : (k < 11 ? 0 : 1); }
+__host__ __device__ constexpr int d0_2(int k) {
+    return k == 0 ? -1 : k == 1 ? 0 : k == 2 ? -1 : k == 3 ? 0 : k == 4 ? 1 : k == 5 ? 0 : 1;
+}
+__host__ __device__ constexpr int d1_2(int k) { return k < 2 ? -1 : (k < 5 ? 0 : 1); }
+
+template <int D> struct Geo;
+template <> struct Geo<3> {
+    static constexpr int W = 15, NT = 4, NE1 = 4, NE2 = 4, B1 = 2, B2 = 2;
+    __host__ __device__ static constexpr int u1(int u) { return u & 1; }
+    __host__ __device__ static constexpr int u2(int u) { return u >> 1; }
+    __host__ __device__ static constexpr int d0(int k) { return d0_3(k); }
+    __host__ __device__ static constexpr int d1(int k) { return d1_3(k); }
+    __host__ __device__ static constexpr int d2(int k) { return d2_3(k); }
+};
+template <> struct Geo<2> {
+    static constexpr int W = 7, NT = 4, NE1 = 6, NE2 = 1, B1 = 4, B2 = 1;
+    __host__ __device__ static constexpr int u1(int u) { return u; }
+    __host__ __device__ static constexpr int u2(int) { return 0; }
+    __host__ __device__ static constexpr int d0(int k) { return d0_2(k); }
+    __host__ __device__ static constexpr int d1(int k) { return d1_2(k); }
+    __host__ __device__ static constexpr int d2(int) { return 0; }
+};
+template <int D>
+__host__ __device__ constexpr bool pair_ok(int s, int u, int k) {
+    using G = Geo<D>;
+    return (s % G::NE1) - 1 == G::u1(u) + G::d1(k) && (s / G::NE1) - (D == 3 ? 1 : 0) == G::u2(u) + G::d2(k);
+}
+template <int D>
+__host__ __device__ constexpr bool src_used(int s) {
+    for (int u = 0; u < Geo<D>::NT; ++u)
+        for (int k = 0; k < Geo<D>::W; ++k)
+            if (pair_ok<D>(s, u, k)) return true;
+    return false;
+}
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, int cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(saddr(b)),
+        "r"(parity)
+        : "memory");
+}
+template <int D>
+__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1, int c2, int c3,
+                                         int c4) {
+    if (D == 3)
+        asm volatile(
+            "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+            "%6}], [%7];" ::"r"(saddr(dst)),
+            "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(saddr(bar))
+            : "memory");
+    else
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+            "%5}], [%6];" ::"r"(saddr(dst)),
+            "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(saddr(bar))
+            : "memory");
+}
+}  // namespace xft
+
+constexpr int XFT_MAXG = 12;
+constexpr int XFT_NST = 4;   // pipeline stages
+struct XftCoef {
+    double c[XFT_MAXG][15];
+};
+struct XftTile {
+    int wl1, wl2, wc, nw;      // warp blocks per tile (axis 1, axis 2), column groups, consumer warps
+    int e1, e2, bc;            // stage box: halo lines (axis 1, axis 2), columns
+    int ntl1, ntl2, nct, nseg, seglen;
+};
+
+template <int D, int NGI>
+__global__ void __launch_bounds__(32 * 17, 1)
+    k_xfanin_tma(const __grid_constant__ CUtensorMap tmap, int nga, int n2, int m, XftTile tl,
+                 const double* __restrict__ tab, const __grid_constant__ XftCoef cint, double* __restrict__ Y) {
+    using G = xft::Geo<D>;
+    constexpr int W = G::W, NT = G::NT, NS = G::NE1 * G::NE2;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    const int stage_elems = tl.e1 * tl.e2 * tl.bc;
+    double* stages = reinterpret_cast<double*>(smraw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smraw + (size_t)XFT_NST * stage_elems * 8);
+    uint64_t* empty = full + XFT_NST;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // CTA -> (line tile, segment, column tile)
+    int bid = blockIdx.x;
+    const int tl1 = bid % tl.ntl1;
+    bid /= tl.ntl1;
+    const int tl2 = bid % tl.ntl2;
+    bid /= tl.ntl2;
+    const int seg = bid % tl.nseg;
+    const int ct = bid / tl.nseg;
+    const int L1 = tl1 * tl.wl1 * G::B1, L2 = tl2 * tl.wl2 * G::B2;   // first target line of the tile
+    const int t0 = seg * tl.seglen, t1 = min(m, t0 + tl.seglen);
+    const int ts = max(t0 - 1, 0), te = min(t1, m - 1);
+    // CTA-level: are all target lines of the tile interior lines?
+    const bool cta_lines_int = L1 >= 1 && L1 + tl.wl1 * G::B1 - 1 <= m - 2 &&
+                               (D == 2 || (L2 >= 1 && L2 + tl.wl2 * G::B2 - 1 <= m - 2));
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < XFT_NST; ++i) {
+            xft::mbar_init(&full[i], 1);
+            xft::mbar_init(&empty[i], tl.nw);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == tl.nw) {
+        // ---------------- producer: one elected lane issues the TMA loads
+        if (lane == 0) {
+            const uint32_t bytes = (uint32_t)stage_elems * 8u;
+            int q = 0;
+            for (int t = ts; t <= te; ++t) {
+                const bool cint_t = cta_lines_int && t >= 2 && t <= m - 3;
+                const int ng = cint_t ? NGI : nga;
+                for (int g = 0; g < ng; ++g, ++q) {
+                    const int b = q % XFT_NST;
+                    if (q >= XFT_NST) xft::mbar_wait(&empty[b], ((q / XFT_NST) - 1) & 1);
+                    xft::mbar_expect_tx(&full[b], bytes);
+                    if (D == 3)
+                        xft::tma_load<3>(stages + (size_t)b * stage_elems, &tmap, &full[b], ct * tl.bc, t, L1 - 1,
+                                         L2 - 1, g);
+                    else
+                        xft::tma_load<2>(stages + (size_t)b * stage_elems, &tmap, &full[b], ct * tl.bc, t, L1 - 1, g,
+                                         0);
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers: warp -> (column group, warp block of lines)
+    const int wc = warp % tl.wc, wl = warp / tl.wc;
+    const int wl1 = wl % tl.wl1, wl2 = wl / tl.wl1;
+    const int col = ct * tl.bc + wc * 32 + lane;
+    const bool cval = col < n2;
+    const int lb1 = wl1 * G::B1, lb2 = wl2 * G::B2;   // warp's first target line inside the tile
+    // stage offsets of the warp's source lines (local halo coordinates)
+    int soff[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        const int le1 = lb1 + (s % G::NE1);                 // (lb1 + e1r + 1), e1r = s%NE1 - 1
+        const int le2 = D == 3 ? lb2 + (s / G::NE1) : 0;
+        soff[s] = (le2 * tl.e1 + le1) * tl.bc + wc * 32 + lane;
+    }
+    int tline[NT], tcls12[NT];
+    bool tval[NT];
+    bool lines_int = true;
+#pragma unroll
+    for (int u = 0; u < NT; ++u) {
+        const int z1 = L1 + lb1 + G::u1(u), z2 = D == 3 ? L2 + lb2 + G::u2(u) : 0;
+        tval[u] = z1 < m && z2 < m;
+        tline[u] = D == 3 ? z1 + m * z2 : z1;
+        const int c1 = z1 == 0 ? 0 : (z1 >= m - 1 ? 2 : 1);
+        const int c2 = z2 == 0 ? 0 : (z2 >= m - 1 ? 2 : 1);
+        tcls12[u] = 3 * c1 + (D == 3 ? 9 * c2 : 0);
+        lines_int &= tval[u] && c1 == 1 && (D == 2 || c2 == 1);
+    }
+    double acc[NT][3];
+#pragma unroll
+    for (int u = 0; u < NT; ++u) acc[u][0] = acc[u][1] = acc[u][2] = 0.0;
+
+    int q = 0;
+    for (int t = ts; t <= te; ++t) {
+        const bool cint_t = cta_lines_int && t >= 2 && t <= m - 3;
+        const bool wint = lines_int && t >= 2 && t <= m - 3;
+        int cb[NT][3];
+#pragma unroll
+        for (int u = 0; u < NT; ++u)
+#pragma unroll
+            for (int w = 0; w < 3; ++w) {
+                const int p = t + w - 1;
+                const int c0 = p <= 0 ? 0 : (p >= m - 1 ? 2 : 1);
+                cb[u][w] = (c0 + tcls12[u]) * nga * W;
+            }
+#pragma unroll
+        for (int g = 0; g < NGI; ++g, ++q) {
+            const int b = q % XFT_NST;
+            xft::mbar_wait(&full[b], (q / XFT_NST) & 1);
+            const double* st = stages + (size_t)b * stage_elems;
+            double src[NS];
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+                if (xft::src_used<D>(s)) src[s] = st[soff[s]];
+            if (wint) {
+#pragma unroll
+                for (int s = 0; s < NS; ++s)
+#pragma unroll
+                    for (int u = 0; u < NT; ++u)
+#pragma unroll
+                        for (int k = 0; k < W; ++k)
+                            if (xft::pair_ok<D>(s, u, k)) {
+                                const int slot = 1 - G::d0(k);
+                                acc[u][slot] = fma(cint.c[g][k], src[s], acc[u][slot]);
+                            }
+            } else {
+                const double* tg = tab + g * W;
+#pragma unroll
+                for (int s = 0; s < NS; ++s)
+#pragma unroll
+                    for (int u = 0; u < NT; ++u)
+#pragma unroll
+                        for (int k = 0; k < W; ++k)
+                            if (xft::pair_ok<D>(s, u, k)) {
+                                const int slot = 1 - G::d0(k);
+                                acc[u][slot] = fma(__ldg(tg + cb[u][slot] + k), src[s], acc[u][slot]);
+                            }
+            }
+            __syncwarp();
+            if (lane == 0) xft::mbar_arrive(&empty[b]);
+        }
+        if (!cint_t) {
+            for (int g = NGI; g < nga; ++g, ++q) {
+                const int b = q % XFT_NST;
+                xft::mbar_wait(&full[b], (q / XFT_NST) & 1);
+                if (!wint) {
+                    const double* st = stages + (size_t)b * stage_elems;
+                    const double* tg = tab + g * W;
+                    double src[NS];
+#pragma unroll
+                    for (int s = 0; s < NS; ++s)
+                        if (xft::src_used<D>(s)) src[s] = st[soff[s]];
+#pragma unroll
+                    for (int s = 0; s < NS; ++s)
+#pragma unroll
+                        for (int u = 0; u < NT; ++u)
+#pragma unroll
+                            for (int k = 0; k < W; ++k)
+                                if (xft::pair_ok<D>(s, u, k)) {
+                                    const int slot = 1 - G::d0(k);
+                                    acc[u][slot] = fma(__ldg(tg + cb[u][slot] + k), src[s], acc[u][slot]);
+                                }
+                }
+                __syncwarp();
+                if (lane == 0) xft::mbar_arrive(&empty[b]);
+            }
+        }
+        // target t-1 complete
+        if (t - 1 >= t0 && cval) {
+#pragma unroll
+            for (int u = 0; u < NT; ++u)
+                if (tval[u]) Y[((long long)(t - 1) + (long long)m * tline[u]) * n2 + col] = acc[u][0];
+        }
+#pragma unroll
+        for (int u = 0; u < NT; ++u) {
+            acc[u][0] = acc[u][1];
+            acc[u][1] = acc[u][2];
+            acc[u][2] = 0.0;
+        }
+    }
+    if (t1 == m && cval) {
+#pragma unroll
+        for (int u = 0; u < NT; ++u)
+            if (tval[u]) Y[((long long)(m - 1) + (long long)m * tline[u]) * n2 + col] = acc[u][0];
+    }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// tile choice: minimise TMA source-line loads per valid target line
+static XftTile choose_tile(int d, int m, int64_t n2, int ngi_total_work_hint) {
+    XftTile best{};
+    double best_cost = 1e30;
+    const int B1 = d == 3 ? 2 : 4;
+    const int lines1 = m, lines2 = d == 3 ? m : 1;
+    for (int wc = 1; wc <= 4; wc *= 2) {
+        if (wc > 1 && n2 < 32LL * wc) continue;
+        for (int w1 = 1; w1 <= 16; ++w1)
+            for (int w2 = 1; w2 <= (d == 3 ? 16 : 1); ++w2) {
+                const int nw = w1 * w2 * wc;
+                if (nw < 4 || nw > 16) continue;
+                const int e1 = w1 * B1 + 2, e2 = d == 3 ? w2 * 2 + 2 : 1;
+                const int bc = 32 * wc;
+                if ((double)e1 * e2 * bc * 8 > 24 * 1024) continue;
+                const int nt1 = (lines1 + w1 * B1 - 1) / (w1 * B1);
+                const int nt2 = d == 3 ? (lines2 + w2 * 2 - 1) / (w2 * 2) : 1;
+                const int64_t nct = (n2 + bc - 1) / bc;
+                const double loads = (double)nt1 * nt2 * e1 * e2 * nct * bc;
+                const double useful = (double)lines1 * lines2 * (double)n2;
+                double cost = loads / useful + 0.02 * (16 - nw) / 16.0;
+                if (cost < best_cost) {
+                    best_cost = cost;
+                    best = XftTile{w1, w2, wc, nw, e1, e2, bc, nt1, nt2, (int)nct, 1, m};
+                }
+            }
+    }
+    (void)ngi_total_work_hint;
+    return best;
+}
+
+int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pitch, const double* Z,
+                      int64_t gstride, double* Y) {
+    if (l1 >= (int)P->xfi_tab.size() || !P->xfi_tab[l1]) return SG_ERR_UNSUPPORTED;
+    const int d = P->fx.d, m = P->fx.lev[l1].m;
+    const int nga = (int)P->vorder.size(), ngi = P->ng_int;
+    if (m < 3 || (pitch & 1) || n1 * n2 >= (1LL << 31) || (d == 3 && ngi != 10) || (d == 2 && ngi != 6))
+        return SG_ERR_UNSUPPORTED;
+    auto enc = get_encode();
+    if (!enc) return SG_ERR_UNSUPPORTED;
+    XftTile tl = choose_tile(d, m, n2, 0);
+    // split the sweep until there are >= 2 CTAs per SM
+    const int64_t base = (int64_t)tl.ntl1 * tl.ntl2 * tl.nct;
+    int seglen = P->xfi_seg > 0 ? P->xfi_seg : m;
+    if (P->xfi_seg <= 0)
+        while (seglen > 8 && base * ((m + seglen - 1) / seglen) < 148 * 3) seglen = (seglen + 1) / 2;
+    tl.seglen = seglen;
+    tl.nseg = (m + seglen - 1) / seglen;
+    const int64_t nblk = base * tl.nseg;
+    if (nblk >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
+
+    CUtensorMap tm;
+    cuuint64_t dims[5], strides[4];
+    cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
+    int rank;
+    if (d == 3) {
+        rank = 5;
+        dims[0] = (cuuint64_t)n2; dims[1] = m; dims[2] = m; dims[3] = m; dims[4] = nga;
+        strides[0] = (cuuint64_t)pitch * 8;
+        strides[1] = (cuuint64_t)pitch * 8 * m;
+        strides[2] = (cuuint64_t)pitch * 8 * m * m;
+        strides[3] = (cuuint64_t)gstride * 8;
+        box[0] = tl.bc; box[1] = 1; box[2] = tl.e1; box[3] = tl.e2; box[4] = 1;
+    } else {
+        rank = 4;
+        dims[0] = (cuuint64_t)n2; dims[1] = m; dims[2] = m; dims[3] = nga;
+        strides[0] = (cuuint64_t)pitch * 8;
+        strides[1] = (cuuint64_t)pitch * 8 * m;
+        strides[2] = (cuuint64_t)gstride * 8;
+        box[0] = tl.bc; box[1] = 1; box[2] = tl.e1; box[3] = 1;
+    }
+    CUresult cr = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double*>(Z), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed");
+        return SG_ERR_CUDA;
+    }
+    XftCoef ci;
+    std::memcpy(ci.c, P->xfi_cint[l1].data(), sizeof(ci.c));
+    const size_t smem = (size_t)XFT_NST * tl.e1 * tl.e2 * tl.bc * 8 + 2 * XFT_NST * sizeof(uint64_t);
+    const int threads = 32 * (tl.nw + 1);
+    const double* tab = P->xfi_tab[l1];
+#define XFT(DD, NG)                                                                                          \
+    do {                                                                                                     \
+        cudaFuncSetAttribute(k_xfanin_tma<DD, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        k_xfanin_tma<DD, NG><<<(unsigned)nblk, threads, smem, P->stream>>>(tm, nga, (int)n2, m, tl, tab, ci, Y); \
+    } while (0)
+    if (d == 3) XFT(3, 10);
+    else XFT(2, 6);
+#undef XFT
+    P->launches++;
+    SG_CUDA(cudaGetLastError());
+    return SG_OK;
+}
+
+}  // namespace sg

@@ -249,7 +249,8 @@ def test_zero_rhs_gives_zero():
     assert it == 1 and float(u.abs().max()) == 0.0
 
 
-@pytest.mark.parametrize("env", ["SG_FUSED", "SG_FORCE_XFIRST", "SG_BRICK", "SG_REG"])
+@pytest.mark.parametrize("env", ["SG_FUSED", "SG_FORCE_XFIRST", "SG_BRICK", "SG_REG", "SG_OLD_XG",
+                                 "SG_XFI_SEG=1", "SG_XFI_SEG=3", "SG_XFI_CPT=2"])
 @pytest.mark.parametrize("name", CONFIG_ORDER)
 def test_apply_strip_operator_kernel_paths(name, env, monkeypatch):
     """Same parity on every kernel path at test sizes: the opt-in fused whole-x
@@ -257,7 +258,8 @@ def test_apply_strip_operator_kernel_paths(name, env, monkeypatch):
     everywhere (large grids pick v-first or x-first by shape)."""
     from oracle.sgrid import SGProblem
     from paper_2204_05988_b200 import Problem
-    monkeypatch.setenv(env, "1")
+    key, _, val = env.partition("=")
+    monkeypatch.setenv(key, val or "1")
     cfg = get_config(name, L=SMALL[name])
     g, o = Problem(cfg), SGProblem(cfg)
     rng = np.random.default_rng(5)
