@@ -68,6 +68,7 @@ extern "C" int sg_create(const sg_config* cfg, void* stream, sg_problem** out) {
     P->use_brick = getenv("SG_BRICK") != nullptr;   // measured 4x slower in round 1: opt-in
     P->use_xfanin = getenv("SG_OLD_XG") == nullptr;
     P->use_xfi_tma = getenv("SG_NO_TMA") == nullptr;
+    P->use_xwhole = getenv("SG_NO_XWHOLE") == nullptr;
     P->xfi_cpt = getenv("SG_XFI_CPT") ? atoi(getenv("SG_XFI_CPT")) : 1;
     P->xfi_seg = getenv("SG_XFI_SEG") ? atoi(getenv("SG_XFI_SEG")) : 0;
     if (cudaStreamCreateWithFlags(&P->gstream, cudaStreamNonBlocking) != cudaSuccess ||

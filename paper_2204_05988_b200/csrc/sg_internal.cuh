@@ -226,9 +226,11 @@ struct sg_problem {
     std::vector<sg::GraphEntry> graphs;
     bool use_xfanin = true;        // line-swept x fan-in pass 2 (SG_OLD_XG disables)
     int xfi_cpt = 1, xfi_seg = 0;
-    bool use_xfi_tma = true;       // TMA-pipelined pass 2 (SG_NO_TMA disables)  // SG_XFI_CPT (columns per lane), SG_XFI_SEG (sweep segment length, 0 auto)
+    bool use_xfi_tma = true;
+    bool use_xwhole = true;        // whole-x pass 2 on tiny x lattices (SG_NO_XWHOLE disables)       // TMA-pipelined pass 2 (SG_NO_TMA disables)  // SG_XFI_CPT (columns per lane), SG_XFI_SEG (sweep segment length, 0 auto)
     std::vector<double*> xfi_tab;  // per x-level: class table [3^d][groups][W] of the combined x matrices
-    std::vector<std::vector<double>> xfi_cint;   // per x-level: interior-class coefficients [12][15]
+    std::vector<std::vector<double>> xfi_cint;
+    std::vector<double*> xw_tab;   // per x-level (tiny lattices): [group][row][k] coefficients   // per x-level: interior-class coefficients [12][15]
     bool use_fused = false;        // opt-in fused whole-x kernel (SG_FUSED)
     int xfirst_mode = 0;           // 0 auto (n1 > n2), 1 never, 2 always (tests)
     int* egrp_dev = nullptr;       // group index of every diag gather entry (fused kernels)
@@ -280,6 +282,8 @@ int launch_xfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const St
 int prepare_xfanin(sg_problem* P);
 int launch_xfanin(sg_problem* P, int l1, int64_t n1, int64_t n2, const double* Z, int64_t gstride, double* Y,
                   double beta);
+int launch_xwhole(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pitch, const double* Z, int64_t gstride,
+                  double* Y);
 // xfanin_tma.cu
 int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pitch, const double* Z,
                       int64_t gstride, double* Y);

@@ -206,7 +206,11 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
     int64_t nnz_x = 0;
     double beta = 0.0;
     int rcx = SG_ERR_UNSUPPORTED;
-    if (tma2) {
+    if (vbox && xbox && P->use_xfanin && P->use_xwhole && !P->use_brick && !P->use_reg && S == 1) {
+        rcx = launch_xwhole(P, g.l1, g.n1, g.n2, pitch, P->wsZ, gstr, Y);
+        if (rcx != SG_OK && rcx != SG_ERR_UNSUPPORTED) return rcx;
+    }
+    if (tma2 && rcx != SG_OK) {
         rcx = launch_xfanin_tma(P, g.l1, g.n1, g.n2, pitch, P->wsZ, gstr, Y);
         if (rcx != SG_OK && rcx != SG_ERR_UNSUPPORTED) return rcx;
         if (rcx == SG_ERR_UNSUPPORTED && pitch != g.n2) {

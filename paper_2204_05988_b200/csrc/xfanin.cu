@@ -337,3 +337,96 @@ int launch_xfanin(sg_problem* P, int l1, int64_t n1, int64_t n2, const double* Z
 }
 
 }  // namespace sg
+
+namespace sg {
+// =====================================================================
+// Whole-x pass 2 for tiny x lattices (m^d <= 27 rows: the level-1 grids):
+// every thread owns one v-column and ALL x-rows in registers; every row has
+// its own boundary class, so the coefficient of (group g, row r, offset k) is
+// c_xw[g][r][k] with (r, k) compile-time and g warp-uniform (uniform constant
+// loads, no L1 traffic), and absent neighbours are dropped at compile time.
+// =====================================================================
+constexpr int XW_MAXG = 16, XW_MAXN = 27, XW_MAXW = 15;
+__constant__ double c_xw[XW_MAXG * XW_MAXN * XW_MAXW];
+
+namespace xw {
+template <int D> __host__ __device__ constexpr int kd(int k, int ax) {
+    return D == 3 ? (ax == 0 ? xfi::d0_3(k) : ax == 1 ? xfi::d1_3(k) : xfi::d2_3(k))
+                  : (ax == 0 ? xfi::d0_2(k) : ax == 1 ? xfi::d1_2(k) : 0);
+}
+template <int D, int M> __host__ __device__ constexpr int nbr(int r, int k) {   // neighbour row or -1
+    int z0 = r % M, z1 = (r / M) % M, z2 = D == 3 ? r / (M * M) : 0;
+    z0 += kd<D>(k, 0);
+    z1 += kd<D>(k, 1);
+    z2 += kd<D>(k, 2);
+    if (z0 < 0 || z0 >= M || z1 < 0 || z1 >= M || (D == 3 && (z2 < 0 || z2 >= M))) return -1;
+    return z0 + M * (z1 + M * z2);
+}
+}  // namespace xw
+
+template <int D, int M>
+__global__ void __launch_bounds__(256, 2) k_xwhole(const double* __restrict__ Z, long long gstride, int nga, int n2,
+                                                   long long pitch, double* __restrict__ Y) {
+    constexpr int N = D == 3 ? M * M * M : M * M;
+    constexpr int W = D == 3 ? 15 : 7;
+    const int col = blockIdx.x * 256 + threadIdx.x;
+    if (col >= n2) return;
+    double acc[N];
+#pragma unroll
+    for (int r = 0; r < N; ++r) acc[r] = 0.0;
+    for (int g = 0; g < nga; ++g) {
+        const double* Zg = Z + g * gstride + col;
+        double z[N];
+#pragma unroll
+        for (int r = 0; r < N; ++r) z[r] = __ldg(Zg + r * pitch);
+        const double* cg = c_xw + g * (N * W);
+#pragma unroll
+        for (int r = 0; r < N; ++r)
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                if (xw::nbr<D, M>(r, k) >= 0) acc[r] = fma(cg[r * W + k], z[xw::nbr<D, M>(r, k)], acc[r]);
+            }
+    }
+#pragma unroll
+    for (int r = 0; r < N; ++r) Y[(long long)r * n2 + col] = acc[r];
+}
+
+int launch_xwhole(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pitch, const double* Z, int64_t gstride,
+                  double* Y) {
+    if (l1 >= (int)P->xfi_tab.size() || !P->xfi_tab[l1]) return SG_ERR_UNSUPPORTED;
+    const int d = P->fx.d, m = P->fx.lev[l1].m, W = P->fx.W;
+    const int nga = (int)P->vorder.size();
+    const bool ok = (d == 3 && m == 3) || (d == 2 && (m == 3 || m == 5));
+    if (!ok || nga > XW_MAXG || n1 * n2 >= (1LL << 31) || n1 > XW_MAXN) return SG_ERR_UNSUPPORTED;
+    if ((int)P->xw_tab.size() <= l1) P->xw_tab.resize(l1 + 1, nullptr);
+    if (!P->xw_tab[l1]) {
+        // [g][r][k] from the class table [cls][g][k]
+        int ncls = 1;
+        for (int q = 0; q < d; ++q) ncls *= 3;
+        std::vector<double> cls((size_t)ncls * nga * W), h((size_t)nga * n1 * W, 0.0);
+        SG_CUDA(cudaMemcpy(cls.data(), P->xfi_tab[l1], sizeof(double) * cls.size(), cudaMemcpyDeviceToHost));
+        for (int r = 0; r < n1; ++r) {
+            int z = r, c = 0, mul = 1;
+            for (int q = 0; q < d; ++q) {
+                const int zq = z % m;
+                z /= m;
+                c += mul * (zq == 0 ? 0 : (zq == m - 1 ? 2 : 1));
+                mul *= 3;
+            }
+            for (int g = 0; g < nga; ++g)
+                for (int k = 0; k < W; ++k) h[((size_t)g * n1 + r) * W + k] = cls[((size_t)c * nga + g) * W + k];
+        }
+        SG_CUDA(cudaMalloc(&P->xw_tab[l1], sizeof(double) * h.size()));
+        SG_CUDA(cudaMemcpy(P->xw_tab[l1], h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+    }
+    SG_CUDA(cudaMemcpyToSymbolAsync(c_xw, P->xw_tab[l1], sizeof(double) * nga * n1 * W, 0, cudaMemcpyDeviceToDevice,
+                                    P->stream));
+    const unsigned blocks = (unsigned)((n2 + 255) / 256);
+    if (d == 3) k_xwhole<3, 3><<<blocks, 256, 0, P->stream>>>(Z, gstride, nga, (int)n2, pitch, Y);
+    else if (m == 3) k_xwhole<2, 3><<<blocks, 256, 0, P->stream>>>(Z, gstride, nga, (int)n2, pitch, Y);
+    else k_xwhole<2, 5><<<blocks, 256, 0, P->stream>>>(Z, gstride, nga, (int)n2, pitch, Y);
+    P->launches++;
+    SG_CUDA(cudaGetLastError());
+    return SG_OK;
+}
+}  // namespace sg
