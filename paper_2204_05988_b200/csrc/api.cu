@@ -69,6 +69,9 @@ extern "C" int sg_create(const sg_config* cfg, void* stream, sg_problem** out) {
     P->use_xfanin = getenv("SG_OLD_XG") == nullptr;
     P->use_xfi_tma = getenv("SG_NO_TMA") == nullptr;
     P->use_xwhole = getenv("SG_NO_XWHOLE") == nullptr;
+    // moment pass 1: faster than the stored-stencil kernel for d = 2 v-lattices, slower for d = 3
+    // (round-1 measurements, profiles/README.md); SG_VMOM forces it on, SG_NO_VMOM off
+    P->use_vmom = getenv("SG_NO_VMOM") == nullptr && (getenv("SG_VMOM") != nullptr || cfg->d == 2);
     P->xfi_cpt = getenv("SG_XFI_CPT") ? atoi(getenv("SG_XFI_CPT")) : 1;
     P->xfi_seg = getenv("SG_XFI_SEG") ? atoi(getenv("SG_XFI_SEG")) : 0;
     if (cudaStreamCreateWithFlags(&P->gstream, cudaStreamNonBlocking) != cudaSuccess ||

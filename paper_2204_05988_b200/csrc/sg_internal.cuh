@@ -230,7 +230,16 @@ struct sg_problem {
     bool use_xwhole = true;        // whole-x pass 2 on tiny x lattices (SG_NO_XWHOLE disables)       // TMA-pipelined pass 2 (SG_NO_TMA disables)  // SG_XFI_CPT (columns per lane), SG_XFI_SEG (sweep segment length, 0 auto)
     std::vector<double*> xfi_tab;  // per x-level: class table [3^d][groups][W] of the combined x matrices
     std::vector<std::vector<double>> xfi_cint;
-    std::vector<double*> xw_tab;   // per x-level (tiny lattices): [group][row][k] coefficients   // per x-level: interior-class coefficients [12][15]
+    std::vector<double*> xw_tab;
+    bool use_vmom = true;          // moment pass 1 (SG_NO_VMOM disables)
+    std::vector<int> vm_ok;        // per v-level: moment tables verified
+    std::vector<double*> vm_tab;   // per v-level: [3^d][10][W] shifted-moment class tables
+    std::vector<std::vector<double>> vm_int;   // per v-level: interior class [10][15]
+    std::vector<int*> vm_blist;    // per v-level: boundary v-nodes
+    std::vector<int> vm_nb;
+    std::vector<int> vm_slot;      // interior group position -> monomial slot
+    int vm_nchi = 0;               // boundary-only groups handled as chi-weighted moments (0: stencil kernel)
+    int vm_chax[6] = {0}, vm_chkeep[6] = {0};   // per x-level (tiny lattices): [group][row][k] coefficients   // per x-level: interior-class coefficients [12][15]
     bool use_fused = false;        // opt-in fused whole-x kernel (SG_FUSED)
     int xfirst_mode = 0;           // 0 auto (n1 > n2), 1 never, 2 always (tests)
     int* egrp_dev = nullptr;       // group index of every diag gather entry (fused kernels)
@@ -284,6 +293,10 @@ int launch_xfanin(sg_problem* P, int l1, int64_t n1, int64_t n2, const double* Z
                   double beta);
 int launch_xwhole(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pitch, const double* Z, int64_t gstride,
                   double* Y);
+// vmoment.cu
+int prepare_vmom(sg_problem* P);
+int launch_vmom(sg_problem* P, int l2, int64_t nrows, int64_t n2, int64_t pitch, const double* X, double* const* outs,
+                const uint8_t* xflag, int64_t n1x);
 // xfanin_tma.cu
 int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pitch, const double* Z,
                       int64_t gstride, double* Y);

@@ -188,7 +188,23 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
             vp.vst[o] = Lv.fst[P->vgroups[P->vorder[o]].spec];
             vp.out[o] = P->wsZ + (int64_t)o * gstr;
         }
-        int rc = P->use_reg ? launch_vfan_reg(P, P->fv.d, S, g.n1, g.n2, Lv.so, Lx.bflag, vp, X) : SG_ERR_UNSUPPORTED;
+        int rc = SG_ERR_UNSUPPORTED;
+        if (!P->use_reg && P->use_vmom) {
+            // interior groups by shifted moments, boundary-only (face) groups by the stencil kernel
+            rc = launch_vmom(P, g.l2, (int64_t)S * g.n1, g.n2, pitch, X, vp.out, Lx.bflag, g.n1);
+            if (rc == SG_OK && nb > P->ng_int && P->vm_nchi == 0) {
+                VfanParams vb;
+                vb.ng = nb - P->ng_int;
+                vb.ng_int = 0;
+                for (int o = 0; o < vb.ng; ++o) {
+                    vb.vst[o] = vp.vst[P->ng_int + o];
+                    vb.out[o] = vp.out[P->ng_int + o];
+                }
+                rc = launch_vfan_st(P, P->fv.d, S, g.n1, g.n2, Lv.so, Lx.bflag, vb, X, pitch);
+            }
+        }
+        if (rc == SG_ERR_UNSUPPORTED && P->use_reg)
+            rc = launch_vfan_reg(P, P->fv.d, S, g.n1, g.n2, Lv.so, Lx.bflag, vp, X);
         if (rc == SG_ERR_UNSUPPORTED) rc = launch_vfan_st(P, P->fv.d, S, g.n1, g.n2, Lv.so, Lx.bflag, vp, X, pitch);
         SG_TRY(rc);
     } else {
@@ -391,6 +407,7 @@ int prepare_stencils(sg_problem* P) {
         SG_CUDA(cudaMemcpy(P->egrp_dev, eg.data(), sizeof(int) * P->egrp_n, cudaMemcpyHostToDevice));
     }
     SG_TRY(prepare_xfanin(P));
+    SG_TRY(prepare_vmom(P));
     SG_CUDA(cudaStreamSynchronize(P->stream));
     return SG_OK;
 }
