@@ -69,6 +69,7 @@ extern "C" int sg_create(const sg_config* cfg, void* stream, sg_problem** out) {
     P->use_xfanin = getenv("SG_OLD_XG") == nullptr;
     P->use_xfi_tma = getenv("SG_NO_TMA") == nullptr;
     P->use_xwhole = getenv("SG_NO_XWHOLE") == nullptr;
+    P->use_cross_batched = getenv("SG_NO_CROSS_BATCH") == nullptr;
     // moment pass 1: faster than the stored-stencil kernel for d = 2 v-lattices, slower for d = 3
     // (round-1 measurements, profiles/README.md); SG_VMOM forces it on, SG_NO_VMOM off
     P->use_vmom = getenv("SG_NO_VMOM") == nullptr && (getenv("SG_VMOM") != nullptr || cfg->d == 2);
@@ -226,6 +227,11 @@ extern "C" void sg_destroy(sg_problem* P) {
                     cudaFree(ce.ctab);
                 }
     cudaFree(P->wsZ); cudaFree(P->wsA); cudaFree(P->wsB); cudaFree(P->wsH); cudaFree(P->red); cudaFree(P->scal);
+    cudaFree(P->cross_q); cudaFree(P->cross_h);
+    for (double* t : P->xfi_tab) cudaFree(t);
+    for (double* t : P->xw_tab) cudaFree(t);
+    for (double* t : P->vm_tab) cudaFree(t);
+    for (int* t : P->vm_blist) cudaFree(t);
     if (P->hscal) cudaFreeHost(P->hscal);
     for (double* v : P->vec) cudaFree(v);
     cudaFree(P->trace_dev);

@@ -920,27 +920,39 @@ __global__ void __launch_bounds__(256) k_jobs(JobList jl) {
     int j = 0;
     while (j + 1 < jl.nj && jl.j[j + 1].blk0 <= (int)blockIdx.x) ++j;
     const Job& J = jl.j[j];
-    const int64_t n1_out = J.dir == 0 ? J.nrows_out : J.n1_in;
-    const int64_t n2_out = J.dir == 1 ? J.nrows_out : J.n2_in;
-    const int64_t per_s = n1_out * n2_out;
-    const int64_t total = per_s * J.S;
+    // 32-bit index arithmetic (every job has < 2^31 outputs, checked on the host)
+    const unsigned n1_out = (unsigned)(J.dir == 0 ? J.nrows_out : J.n1_in);
+    const unsigned n2_out = (unsigned)(J.dir == 1 ? J.nrows_out : J.n2_in);
+    const unsigned per_s = n1_out * n2_out;
+    const unsigned total = per_s * (unsigned)J.S;
+    const unsigned nrows = (unsigned)J.nrows_out;
+    const unsigned n1i = (unsigned)J.n1_in, n2i = (unsigned)J.n2_in;
     const int nblk = (j + 1 < jl.nj ? jl.j[j + 1].blk0 : jl.total_blocks) - J.blk0;
-    for (int64_t t = (int64_t)(blockIdx.x - J.blk0) * blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)nblk * blockDim.x) {
-        const int s = (int)(t / per_s);
-        const int64_t rc = t - s * per_s;
-        const int64_t r = rc / n2_out, c = rc - r * n2_out;
-        const int64_t row = J.dir == 1 ? c : r;
-        const int64_t nrows = J.nrows_out;
+    const int W = J.W;
+    for (unsigned t = (unsigned)(blockIdx.x - J.blk0) * blockDim.x + threadIdx.x; t < total;
+         t += (unsigned)nblk * blockDim.x) {
+        const unsigned s = t >= per_s ? 1u : 0u;   // S <= 2
+        const unsigned rc = t - s * per_s;
+        const unsigned r = rc / n2_out, c = rc - r * n2_out;
         double acc = 0.0;
-        for (int k = 0; k < J.W; ++k) {
-            const int32_t col = __ldg(J.cols + k * nrows + row);
-            if (col < 0) continue;
-            const double x = J.dir == 1 ? __ldg(J.in + ((int64_t)s * J.n1_in + r) * J.n2_in + col)
-                                        : __ldg(J.in + ((int64_t)s * J.n1_in + col) * J.n2_in + c);
-            acc = fma(__ldg(J.vals + k * nrows + row), x, acc);
+        if (J.dir == 1) {
+            const double* in = J.in + ((size_t)s * n1i + r) * n2i;
+            for (int k = 0; k < W; ++k) {
+                const int32_t col = __ldg(J.cols + k * nrows + c);
+                if (col >= 0) acc = fma(__ldg(J.vals + k * nrows + c), __ldg(in + col), acc);
+            }
+        } else {
+            const double* in = J.in + (size_t)s * n1i * n2i + c;
+            for (int k = 0; k < W; ++k) {
+                const int32_t col = __ldg(J.cols + k * nrows + r);
+                if (col >= 0) acc = fma(__ldg(J.vals + k * nrows + r), __ldg(in + (size_t)col * n2i), acc);
+            }
         }
-        J.out[t] = (J.add ? J.add[t] : 0.0) + J.scale * acc;
+        const double v = (J.add ? J.add[t] : 0.0) + J.scale * acc;
+        if (J.opitch > 0)
+            J.out[((size_t)s * n1_out + r) * (size_t)J.opitch + c] = v;
+        else
+            J.out[t] = v;
     }
 }
 
@@ -956,6 +968,10 @@ int launch_jobs(sg_problem* P, std::vector<Job>& jobs) {
             const int64_t n2_out = J.dir == 1 ? J.nrows_out : J.n2_in;
             const int64_t total = n1_out * n2_out * J.S;
             if (total == 0) continue;
+            if (total >= (1LL << 31) || J.S > 2) {
+                set_error("transfer job too large for 32-bit indexing");
+                return SG_ERR_UNSUPPORTED;
+            }
             J.blk0 = blk;
             blk += (int)std::min<int64_t>((total + 2047) / 2048, 148 * 8);
             jl.j[jl.nj++] = J;

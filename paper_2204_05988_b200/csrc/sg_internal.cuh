@@ -149,6 +149,7 @@ struct Job {
     int64_t n1_in, n2_in, nrows_out;
     double scale;
     int S, dir, W, blk0;
+    int64_t opitch = 0;   // output row pitch (0: natural n2_out)
 };
 struct JobList {
     int nj, total_blocks;
@@ -231,6 +232,10 @@ struct sg_problem {
     std::vector<double*> xfi_tab;  // per x-level: class table [3^d][groups][W] of the combined x matrices
     std::vector<std::vector<double>> xfi_cint;
     std::vector<double*> xw_tab;
+    double* cross_q = nullptr;     // batched cross-grid lower part: stage-0 fan-outs of all v-groups
+    double* cross_h = nullptr;     //   and the Horner results per target and group (even pitch)
+    bool cross_batched_tried = false;
+    bool use_cross_batched = true; // SG_NO_CROSS_BATCH disables
     bool use_vmom = true;          // moment pass 1 (SG_NO_VMOM disables)
     std::vector<int> vm_ok;        // per v-level: moment tables verified
     std::vector<double*> vm_tab;   // per v-level: [3^d][10][W] shifted-moment class tables
@@ -302,6 +307,7 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
                       int64_t gstride, double* Y);
 // solver.cu
 int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y);
+int pass1_vgroups(sg_problem* P, int l1, int l2, const double* X, double* const* outs, int64_t pitch);
 int apply_cross(sg_problem* P, const std::vector<Term>* terms_override, const double* Tb, int S_out, int S_in,
                 const double* X, double* Y);
 int64_t set_size(const sg_problem* P, int set, int S);

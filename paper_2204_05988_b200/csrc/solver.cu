@@ -71,6 +71,70 @@ static bool l_has_xfi(const sg_problem* P, int l1) {
            ((P->fx.d == 3 && P->ng_int == 10) || (P->fx.d == 2 && P->ng_int == 6)) && P->fx.lev[l1].m >= 3;
 }
 
+// pass 1 of the per-grid operator on grid (l1, l2): Z_o = (Id x Id x B_o) X for every v-group o
+// (vorder; boundary-only groups on x-boundary rows only), written with row pitch `pitch`
+int pass1_vgroups(sg_problem* P, int l1, int l2, const double* X, double* const* outs, int64_t pitch) {
+    const int S = P->S;
+    const Level& Lx = P->fx.lev[l1];
+    const Level& Lv = P->fv.lev[l2];
+    const int64_t n1 = Lx.n, n2 = Lv.n;
+    const int nb = (int)P->vorder.size();
+    const bool vbox = P->fv.kind == SG_MESH_BOX && nb <= MAXG;
+    if (vbox) {
+        VfanParams vp;
+        vp.ng = nb;
+        vp.ng_int = P->ng_int;
+        for (int o = 0; o < nb; ++o) {
+            vp.vst[o] = Lv.fst[P->vgroups[P->vorder[o]].spec];
+            vp.out[o] = outs[o];
+        }
+        int rc = SG_ERR_UNSUPPORTED;
+        if (!P->use_reg && P->use_vmom) {
+            // interior groups by shifted moments, boundary-only (face) groups by the stencil kernel
+            rc = launch_vmom(P, l2, (int64_t)S * n1, n2, pitch, X, vp.out, Lx.bflag, n1);
+            if (rc == SG_OK && nb > P->ng_int && P->vm_nchi == 0) {
+                VfanParams vb;
+                vb.ng = nb - P->ng_int;
+                vb.ng_int = 0;
+                for (int o = 0; o < vb.ng; ++o) {
+                    vb.vst[o] = vp.vst[P->ng_int + o];
+                    vb.out[o] = vp.out[P->ng_int + o];
+                }
+                rc = launch_vfan_st(P, P->fv.d, S, n1, n2, Lv.so, Lx.bflag, vb, X, pitch);
+            }
+        }
+        if (rc == SG_ERR_UNSUPPORTED && P->use_reg) rc = launch_vfan_reg(P, P->fv.d, S, n1, n2, Lv.so, Lx.bflag, vp, X);
+        if (rc == SG_ERR_UNSUPPORTED) rc = launch_vfan_st(P, P->fv.d, S, n1, n2, Lv.so, Lx.bflag, vp, X, pitch);
+        return rc;
+    }
+    if (pitch != n2) return SG_ERR_UNSUPPORTED;
+    for (int b0 = 0; b0 < nb; b0 += MAX_FANOUT) {
+        FanoutList fl;
+        fl.no = std::min(MAX_FANOUT, nb - b0);
+        for (int o = 0; o < fl.no; ++o) {
+            fl.vals[o] = Lv.fm[P->vgroups[P->vorder[b0 + o]].spec];
+            fl.out[o] = outs[b0 + o];
+        }
+        SG_TRY(launch_fanout(P, 1, P->fv.W, S, n1, n2, n2, Lv.cols, X, fl));
+    }
+    return SG_OK;
+}
+
+// pass 2 on grid (l1, l2) over all v-groups (vorder) from intermediates with group stride gstr:
+// Y = sum_o C_o Z_o with the line-swept kernels; SG_ERR_UNSUPPORTED if they do not cover it
+static int pass2_fast(sg_problem* P, int l1, int l2, const double* Z, int64_t pitch, int64_t gstr, double* Y) {
+    const int64_t n1 = P->fx.lev[l1].n, n2 = P->fv.lev[l2].n;
+    if (P->fx.kind != SG_MESH_BOX || P->fv.kind != SG_MESH_BOX || P->S != 1 || !P->use_xfanin || P->use_brick ||
+        P->use_reg)
+        return SG_ERR_UNSUPPORTED;
+    int rc = SG_ERR_UNSUPPORTED;
+    if (P->use_xwhole) rc = launch_xwhole(P, l1, n1, n2, pitch, Z, gstr, Y);
+    if (rc == SG_ERR_UNSUPPORTED && P->use_xfi_tma && (pitch & 1) == 0 && l_has_xfi(P, l1))
+        rc = launch_xfanin_tma(P, l1, n1, n2, pitch, Z, gstr, Y);
+    if (rc == SG_ERR_UNSUPPORTED && pitch == n2) rc = launch_xfanin(P, l1, n1, n2, Z, gstr, Y, 0.0);
+    return rc;
+}
+
 // ------------------------------------------------ diagonal block (one grid)
 // Y = sum_t T_t (x) A_t (x) B_t X, grouped by the v-spec b:
 //   Z_b = (Id x Id x B_b) X           (fanout along v, one read of X per 4 b's)
@@ -180,43 +244,10 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
         set_error("apply_diag: workspace too small");
         return SG_ERR_STATE;
     }
-    if (vbox) {
-        VfanParams vp;
-        vp.ng = nb;
-        vp.ng_int = P->ng_int;
-        for (int o = 0; o < nb; ++o) {
-            vp.vst[o] = Lv.fst[P->vgroups[P->vorder[o]].spec];
-            vp.out[o] = P->wsZ + (int64_t)o * gstr;
-        }
-        int rc = SG_ERR_UNSUPPORTED;
-        if (!P->use_reg && P->use_vmom) {
-            // interior groups by shifted moments, boundary-only (face) groups by the stencil kernel
-            rc = launch_vmom(P, g.l2, (int64_t)S * g.n1, g.n2, pitch, X, vp.out, Lx.bflag, g.n1);
-            if (rc == SG_OK && nb > P->ng_int && P->vm_nchi == 0) {
-                VfanParams vb;
-                vb.ng = nb - P->ng_int;
-                vb.ng_int = 0;
-                for (int o = 0; o < vb.ng; ++o) {
-                    vb.vst[o] = vp.vst[P->ng_int + o];
-                    vb.out[o] = vp.out[P->ng_int + o];
-                }
-                rc = launch_vfan_st(P, P->fv.d, S, g.n1, g.n2, Lv.so, Lx.bflag, vb, X, pitch);
-            }
-        }
-        if (rc == SG_ERR_UNSUPPORTED && P->use_reg)
-            rc = launch_vfan_reg(P, P->fv.d, S, g.n1, g.n2, Lv.so, Lx.bflag, vp, X);
-        if (rc == SG_ERR_UNSUPPORTED) rc = launch_vfan_st(P, P->fv.d, S, g.n1, g.n2, Lv.so, Lx.bflag, vp, X, pitch);
-        SG_TRY(rc);
-    } else {
-        for (int b0 = 0; b0 < nb; b0 += MAX_FANOUT) {
-            FanoutList fl;
-            fl.no = std::min(MAX_FANOUT, nb - b0);
-            for (int o = 0; o < fl.no; ++o) {
-                fl.vals[o] = Lv.fm[P->vgroups[P->vorder[b0 + o]].spec];
-                fl.out[o] = P->wsZ + (int64_t)(b0 + o) * S * n;
-            }
-            SG_TRY(launch_fanout(P, 1, P->fv.W, S, g.n1, g.n2, g.n2, Lv.cols, X, fl));
-        }
+    {
+        std::vector<double*> outs(nb);
+        for (int o = 0; o < nb; ++o) outs[o] = P->wsZ + (int64_t)o * gstr;
+        SG_TRY(pass1_vgroups(P, g.l1, g.l2, X, outs.data(), pitch));
     }
     // ---- pass 2: Y = sum_b sum_{s,s'} (e_s e_s'^T (x) C_b^{ss'} (x) Id) Z_b
     int64_t nnz_x = 0;
@@ -423,6 +454,7 @@ int prepare_stencils(sg_problem* P) {
 //  upper part (l1 < l1'): per x-group a symmetric with the roles of x, v swapped.
 // "mass" mode (Tb != nullptr): single term Tb (x) M^x (x) M^v, S_out x S_in.
 static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in, const double* X, double* Y);
+static int cross_lower_batched(sg_problem* P, const double* X, double* Y);
 
 // The cross-grid apply is a fixed sequence of ~10^3 small launches (transfer
 // chains per group); it is captured once per (X, Y, Tb) into a CUDA graph on the
@@ -430,6 +462,11 @@ static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in
 // (dominant on the 2D configurations).
 int apply_cross(sg_problem* P, const std::vector<Term>* /*unused*/, const double* Tb, int S_out, int S_in,
                 const double* X, double* Y) {
+    if (!P->cross_batched_tried && !Tb) {
+        int rc = cross_lower_batched(P, nullptr, nullptr);   // allocation only (never inside a capture)
+        if (rc != SG_OK && rc != SG_ERR_UNSUPPORTED) return rc;
+        P->cross_batched_tried = true;
+    }
     if (!P->use_graphs) return apply_cross_impl(P, Tb, S_out, S_in, X, Y);
     GraphKey key;
     key.X = X;
@@ -476,6 +513,119 @@ int apply_cross(sg_problem* P, const std::vector<Term>* /*unused*/, const double
     return SG_OK;
 }
 
+
+// Batched lower part of the cross-grid apply (see apply_cross_impl), S = 1 box lattices only.
+// Memory: Q0 = stage-0 fan-outs of every group at every source (natural pitch), H = Horner
+// results of every group at every target (even pitch, TMA-readable), both allocated once.
+static int cross_lower_batched(sg_problem* P, const double* X, double* Y) {
+    if (!P->use_cross_batched || P->S != 1 || P->fx.kind != SG_MESH_BOX || P->fv.kind != SG_MESH_BOX || P->fx.d < 2 ||
+        !P->use_xfanin || P->use_brick || P->use_reg)
+        return SG_ERR_UNSUPPORTED;
+    const auto& A = P->active;
+    const int ng = (int)A.size();
+    const int L = P->cfg.L;
+    const int nga = (int)P->vorder.size();
+    const int Wv = P->fv.W;
+    auto n1 = [&](int l) { return P->fx.lev[l].n; };
+    auto n2 = [&](int l) { return P->fv.lev[l].n; };
+    auto pit = [&](int l) { return n2(l) + (n2(l) & 1); };
+    // every target must be covered by the fast gathers
+    for (int p = 1; p <= ng; ++p) {
+        const int m = P->fx.lev[p].m;
+        const bool whole = P->use_xwhole && ((P->fx.d == 3 && m == 3) || (P->fx.d == 2 && (m == 3 || m == 5))) &&
+                           nga <= 16 && p < (int)P->xfi_tab.size() && P->xfi_tab[p];
+        if (!whole && (p == 1 || !(P->use_xfi_tma && l_has_xfi(P, p)))) return SG_ERR_UNSUPPORTED;
+    }
+    std::vector<int64_t> qo(ng + 2, 0), ho(ng + 2, 0);
+    for (int p = 1; p <= ng; ++p) {
+        qo[p + 1] = qo[p] + (int64_t)nga * n1(p) * n2(L - p);
+        ho[p + 1] = ho[p] + (int64_t)nga * n1(p) * pit(L - p);
+    }
+    if (!P->cross_batched_tried) {
+        // first use: allocate outside any stream capture (apply_cross calls us uncaptured first)
+        P->cross_batched_tried = true;
+        if (cudaMalloc(&P->cross_q, sizeof(double) * qo[ng + 1]) != cudaSuccess ||
+            cudaMalloc(&P->cross_h, sizeof(double) * ho[ng + 1]) != cudaSuccess) {
+            cudaGetLastError();
+            cudaFree(P->cross_q);
+            cudaFree(P->cross_h);
+            P->cross_q = P->cross_h = nullptr;
+            if (P->verbose) fprintf(stderr, "[sg] batched cross-grid apply: not enough memory, per-group path\n");
+            return SG_ERR_UNSUPPORTED;
+        }
+        // finite contents for rows a boundary-only group never writes (they meet zero coefficients)
+        SG_CUDA(cudaMemset(P->cross_q, 0, sizeof(double) * qo[ng + 1]));
+        SG_CUDA(cudaMemset(P->cross_h, 0, sizeof(double) * ho[ng + 1]));
+        SG_CUDA(cudaDeviceSynchronize());
+        return SG_OK;   // allocation-only call
+    }
+    if (!P->cross_q || !P->cross_h) return SG_ERR_UNSUPPORTED;
+    auto Q0 = [&](int pp, int o) { return P->cross_q + qo[pp] + (int64_t)o * n1(pp) * n2(L - pp); };
+    auto H = [&](int p, int o) { return P->cross_h + ho[p] + (int64_t)o * n1(p) * pit(L - p); };
+    // 1. stage-0 fan-out of all groups at every source: Q0[pp][o] = (Id x B_o) X_pp
+    for (int pp = 1; pp <= ng; ++pp) {
+        std::vector<double*> outs(nga);
+        for (int o = 0; o < nga; ++o) outs[o] = Q0(pp, o);
+        SG_TRY(pass1_vgroups(P, pp, L - pp, X + A[pp - 1].off1, outs.data(), n2(L - pp)));
+    }
+    // 2./3. per group: restriction chains in v and Horner prolongation in x; the last
+    // Horner stage of target p (m = p) writes H[p][o] with the even pitch
+    std::vector<std::vector<int64_t>> qoff(ng);
+    for (int o = 0; o < nga; ++o) {
+        int64_t pos = 0;
+        for (int pp = 1; pp <= ng; ++pp) {
+            qoff[pp - 1].assign(ng - pp + 1, 0);
+            for (int k = 1; k <= ng - pp; ++k) {
+                qoff[pp - 1][k] = pos;
+                pos += n1(pp) * n2(L - pp - k);
+            }
+        }
+        if ((size_t)pos > P->wsZ_n) {
+            set_error("apply_cross: chain workspace too small");
+            return SG_ERR_STATE;
+        }
+        auto Q = [&](int pp, int k) -> double* { return k == 0 ? Q0(pp, o) : P->wsZ + qoff[pp - 1][k]; };
+        for (int k = 1; k <= ng - 1; ++k) {
+            std::vector<Job> jobs;
+            for (int pp = 1; pp <= ng - k; ++pp) {
+                const int lv0 = L - pp, lf = lv0 - k + 1, lc = lv0 - k;
+                jobs.push_back({Q(pp, k - 1), nullptr, Q(pp, k), P->fv.lev[lf].rcols, P->fv.lev[lf].rvals, n1(pp), n2(lf),
+                                n2(lc), 1.0, 1, 1, Wv, 0});
+            }
+            SG_TRY(launch_jobs(P, jobs));
+        }
+        double* hb[2] = {P->wsH, P->wsH + set_size(P, SG_SET_ACTIVE, 1)};
+        for (int m = 2; m <= ng; ++m) {
+            std::vector<Job> jobs;
+            for (int p = m; p <= ng; ++p) {
+                const int lv = L - p;
+                const double* in = m == 2 ? Q(1, p - 1) : hb[(m - 1) & 1] + A[p - 1].off1;
+                Job J{in, Q(m, p - m), hb[m & 1] + A[p - 1].off1, P->fx.lev[m].pcols, P->fx.lev[m].pvals, n1(m - 1), n2(lv),
+                      n1(m), 1.0, 1, 0, 2, 0};
+                if (p == m) {
+                    J.out = H(p, o);
+                    J.opitch = pit(lv);
+                }
+                jobs.push_back(J);
+            }
+            SG_TRY(launch_jobs(P, jobs));
+        }
+    }
+    // 4. one gather over all groups per target: Y_p = sum_o C_o^{(p)} H[p][o]
+    for (int p = 1; p <= ng; ++p) {
+        const int lv = L - p;
+        const double* base = p == 1 ? Q0(1, 0) : H(p, 0);
+        const int64_t pitch = p == 1 ? n2(lv) : pit(lv);
+        const int64_t gstr = p == 1 ? n1(1) * n2(lv) : n1(p) * pit(lv);
+        int rc = pass2_fast(P, p, lv, base, pitch, gstr, Y + A[p - 1].off1);
+        if (rc != SG_OK) {
+            if (rc == SG_ERR_UNSUPPORTED) set_error("apply_cross: batched gather unsupported after setup");
+            return rc == SG_ERR_UNSUPPORTED ? SG_ERR_STATE : rc;
+        }
+    }
+    return SG_OK;
+}
+
 static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in, const double* X, double* Y) {
     const bool mass = Tb != nullptr;
     const auto& A = P->active;
@@ -494,7 +644,16 @@ static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in
     // chain buffer layout: Q[p'][k], p' = 1..ng (index p'-1), k = 0..(#targets-1)
     std::vector<std::vector<int64_t>> qoff(ng);
     // ---------------- lower part
-    const int nvg = mass ? 1 : (int)P->vgroups.size();
+    // batched variant: all v-groups fanned out at once per source, per-group restriction
+    // chains and Horner prolongation, and ONE line-swept x gather over all groups per target
+    // (PAPER.md l.506-516 with A_{l,l'} = A_l E; same arithmetic, fewer passes over Y and X)
+    bool lower_done = false;
+    if (!mass) {
+        int rc = cross_lower_batched(P, X, Y);
+        if (rc == SG_OK) lower_done = true;
+        else if (rc != SG_ERR_UNSUPPORTED) return rc;
+    }
+    const int nvg = lower_done ? 0 : (mass ? 1 : (int)P->vgroups.size());
     for (int b = 0; b < nvg; ++b) {
         const int vspec = mass ? P->mass_v : P->vgroups[b].spec;
         int64_t pos = 0;

@@ -241,6 +241,8 @@ __global__ void __launch_bounds__(256, CPT == 1 ? 2 : 1)
     if (t1 == m) flush(m - 1);
 }
 
+int prepare_xwhole(sg_problem* P);
+
 // host: class tables of the combined x matrices of every v-group (vorder) per x-level
 int prepare_xfanin(sg_problem* P) {
     P->xfi_tab.assign(P->F + 1, nullptr);
@@ -279,6 +281,7 @@ int prepare_xfanin(sg_problem* P) {
             for (int k = 0; k < W; ++k) ci[o * 15 + k] = h[((size_t)icls * nga + o) * W + k];
         P->xfi_cint[l] = ci;
     }
+    SG_TRY(prepare_xwhole(P));
     return SG_OK;
 }
 
@@ -391,16 +394,18 @@ __global__ void __launch_bounds__(256, 2) k_xwhole(const double* __restrict__ Z,
     for (int r = 0; r < N; ++r) Y[(long long)r * n2 + col] = acc[r];
 }
 
-int launch_xwhole(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pitch, const double* Z, int64_t gstride,
-                  double* Y) {
-    if (l1 >= (int)P->xfi_tab.size() || !P->xfi_tab[l1]) return SG_ERR_UNSUPPORTED;
-    const int d = P->fx.d, m = P->fx.lev[l1].m, W = P->fx.W;
+// [g][r][k] coefficient tables of the tiny x-levels (setup time: never allocate inside a capture)
+int prepare_xwhole(sg_problem* P) {
+    P->xw_tab.assign(P->F + 1, nullptr);
+    const int d = P->fx.d, W = P->fx.W;
     const int nga = (int)P->vorder.size();
-    const bool ok = (d == 3 && m == 3) || (d == 2 && (m == 3 || m == 5));
-    if (!ok || nga > XW_MAXG || n1 * n2 >= (1LL << 31) || n1 > XW_MAXN) return SG_ERR_UNSUPPORTED;
-    if ((int)P->xw_tab.size() <= l1) P->xw_tab.resize(l1 + 1, nullptr);
-    if (!P->xw_tab[l1]) {
-        // [g][r][k] from the class table [cls][g][k]
+    if (nga > XW_MAXG) return SG_OK;
+    for (int l1 = 1; l1 <= P->F && l1 < (int)P->xfi_tab.size(); ++l1) {
+        if (!P->xfi_tab[l1]) continue;
+        const int m = P->fx.lev[l1].m;
+        const int64_t n1 = P->fx.lev[l1].n;
+        const bool ok = (d == 3 && m == 3) || (d == 2 && (m == 3 || m == 5));
+        if (!ok || n1 > XW_MAXN) continue;
         int ncls = 1;
         for (int q = 0; q < d; ++q) ncls *= 3;
         std::vector<double> cls((size_t)ncls * nga * W), h((size_t)nga * n1 * W, 0.0);
@@ -419,6 +424,17 @@ int launch_xwhole(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pitch, 
         SG_CUDA(cudaMalloc(&P->xw_tab[l1], sizeof(double) * h.size()));
         SG_CUDA(cudaMemcpy(P->xw_tab[l1], h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
     }
+    return SG_OK;
+}
+
+int launch_xwhole(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pitch, const double* Z, int64_t gstride,
+                  double* Y) {
+    if (l1 >= (int)P->xfi_tab.size() || !P->xfi_tab[l1]) return SG_ERR_UNSUPPORTED;
+    const int d = P->fx.d, m = P->fx.lev[l1].m, W = P->fx.W;
+    const int nga = (int)P->vorder.size();
+    const bool ok = (d == 3 && m == 3) || (d == 2 && (m == 3 || m == 5));
+    if (!ok || nga > XW_MAXG || n1 * n2 >= (1LL << 31) || n1 > XW_MAXN) return SG_ERR_UNSUPPORTED;
+    if (l1 >= (int)P->xw_tab.size() || !P->xw_tab[l1]) return SG_ERR_UNSUPPORTED;   // built in prepare_xfanin
     SG_CUDA(cudaMemcpyToSymbolAsync(c_xw, P->xw_tab[l1], sizeof(double) * nga * n1 * W, 0, cudaMemcpyDeviceToDevice,
                                     P->stream));
     const unsigned blocks = (unsigned)((n2 + 255) / 256);

@@ -120,6 +120,26 @@ def test_apply_full_cross_grid(name):
         assert relmax(Y[l], ref[l]) <= 1e-12, l
 
 
+@pytest.mark.parametrize("env", ["SG_NO_CROSS_BATCH", "SG_NO_TMA", "SG_VMOM"])
+@pytest.mark.parametrize("name", ["c2_4d_stream", "c4_6d_stream"])
+def test_apply_full_cross_grid_paths(name, env, monkeypatch):
+    """Cross-grid apply on the per-group path and with the batched lower part's kernel variants."""
+    from oracle.sgrid import SGProblem
+    from paper_2204_05988_b200 import Problem
+    monkeypatch.setenv(env, "1")
+    cfg = get_config(name, L=SMALL[name])
+    g, o = Problem(cfg), SGProblem(cfg)
+    rng = np.random.default_rng(11)
+    U = {l: rng.standard_normal(o.shape(l)) for l in o.active}
+    Xt = from_blocks(g, U)
+    Yt = torch.zeros_like(Xt)
+    g.sg_apply_full(Xt, Yt)
+    Y = to_blocks(g, Yt)
+    ref = o.apply_full(o.terms, U)
+    for l in o.active:
+        assert relmax(Y[l], ref[l]) <= 1e-12, l
+
+
 @pytest.mark.parametrize("name", ["c1_2d_rot", "c3_4d_lshape", "c4_6d_stream"])
 def test_apply_mass_full(name):
     from oracle.problem import mass_terms
@@ -250,7 +270,7 @@ def test_zero_rhs_gives_zero():
 
 
 @pytest.mark.parametrize("env", ["SG_FUSED", "SG_FORCE_XFIRST", "SG_BRICK", "SG_REG", "SG_OLD_XG",
-                                 "SG_XFI_SEG=1", "SG_XFI_SEG=3", "SG_XFI_CPT=2", "SG_NO_TMA", "SG_NO_XWHOLE", "SG_NO_VMOM", "SG_VMOM"])
+                                 "SG_XFI_SEG=1", "SG_XFI_SEG=3", "SG_XFI_CPT=2", "SG_NO_TMA", "SG_NO_XWHOLE", "SG_NO_VMOM", "SG_VMOM", "SG_NO_CROSS_BATCH"])
 @pytest.mark.parametrize("name", CONFIG_ORDER)
 def test_apply_strip_operator_kernel_paths(name, env, monkeypatch):
     """Same parity on every kernel path at test sizes: the opt-in fused whole-x
