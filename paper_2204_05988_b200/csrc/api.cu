@@ -229,8 +229,9 @@ extern "C" void sg_destroy(sg_problem* P) {
     cudaFree(P->wsZ); cudaFree(P->wsA); cudaFree(P->wsB); cudaFree(P->wsH); cudaFree(P->red); cudaFree(P->scal);
     cudaFree(P->cross_q); cudaFree(P->cross_h);
     for (double* t : P->xfi_tab) cudaFree(t);
-    for (double* t : P->xw_tab) cudaFree(t);
+    for (double* t : P->xfi_itab) cudaFree(t);
     for (double* t : P->vm_tab) cudaFree(t);
+    for (double* t : P->xw_dev) cudaFree(t);
     for (int* t : P->vm_blist) cudaFree(t);
     if (P->hscal) cudaFreeHost(P->hscal);
     for (double* v : P->vec) cudaFree(v);

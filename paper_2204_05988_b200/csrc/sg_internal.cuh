@@ -229,9 +229,12 @@ struct sg_problem {
     int xfi_cpt = 1, xfi_seg = 0;
     bool use_xfi_tma = true;
     bool use_xwhole = true;        // whole-x pass 2 on tiny x lattices (SG_NO_XWHOLE disables)       // TMA-pipelined pass 2 (SG_NO_TMA disables)  // SG_XFI_CPT (columns per lane), SG_XFI_SEG (sweep segment length, 0 auto)
+    std::vector<double*> xfi_itab; // per x-level: interior groups only [3^d][ng_int][W]
     std::vector<double*> xfi_tab;  // per x-level: class table [3^d][groups][W] of the combined x matrices
     std::vector<std::vector<double>> xfi_cint;
-    std::vector<double*> xw_tab;
+    std::vector<double*> xw_tab;   // per x-level (tiny lattices): non-null when the whole-x tables exist
+    std::vector<double*> xw_dev;   // per x-level: compact [group][pair] coefficient table (device)
+    std::vector<int> xw_np;
     double* cross_q = nullptr;     // batched cross-grid lower part: stage-0 fan-outs of all v-groups
     double* cross_h = nullptr;     //   and the Horner results per target and group (even pitch)
     bool cross_batched_tried = false;

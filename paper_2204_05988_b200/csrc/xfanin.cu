@@ -246,6 +246,7 @@ int prepare_xwhole(sg_problem* P);
 // host: class tables of the combined x matrices of every v-group (vorder) per x-level
 int prepare_xfanin(sg_problem* P) {
     P->xfi_tab.assign(P->F + 1, nullptr);
+    P->xfi_itab.assign(P->F + 1, nullptr);
     P->xfi_cint.assign(P->F + 1, {});
     if (P->fx.kind != SG_MESH_BOX || P->S != 1 || P->fx.d < 2 || !P->use_classes) return SG_OK;
     const int nga = (int)P->vorder.size();
@@ -276,6 +277,15 @@ int prepare_xfanin(sg_problem* P) {
         SG_CUDA(cudaMalloc(&dt, sizeof(double) * h.size()));
         SG_CUDA(cudaMemcpy(dt, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
         P->xfi_tab[l] = dt;
+        {
+            std::vector<double> hi((size_t)ncls * P->ng_int * W);
+            for (int c = 0; c < ncls; ++c)
+                for (int o = 0; o < P->ng_int; ++o)
+                    for (int k = 0; k < W; ++k)
+                        hi[((size_t)c * P->ng_int + o) * W + k] = h[((size_t)c * nga + o) * W + k];
+            SG_CUDA(cudaMalloc(&P->xfi_itab[l], sizeof(double) * std::max<size_t>(hi.size(), 1)));
+            SG_CUDA(cudaMemcpy(P->xfi_itab[l], hi.data(), sizeof(double) * hi.size(), cudaMemcpyHostToDevice));
+        }
         std::vector<double> ci((size_t)XFI_MAXG * 15, 0.0);
         for (int o = 0; o < P->ng_int; ++o)
             for (int k = 0; k < W; ++k) ci[o * 15 + k] = h[((size_t)icls * nga + o) * W + k];
@@ -350,7 +360,7 @@ namespace sg {
 // loads, no L1 traffic), and absent neighbours are dropped at compile time.
 // =====================================================================
 constexpr int XW_MAXG = 16, XW_MAXN = 27, XW_MAXW = 15;
-__constant__ double c_xw[XW_MAXG * XW_MAXN * XW_MAXW];
+constexpr int XW_MAXP = 223;   // valid (row, offset) pairs of the 3^3 lattice (3^2: 41, 5^2: 137)
 
 namespace xw {
 template <int D> __host__ __device__ constexpr int kd(int k, int ax) {
@@ -365,13 +375,27 @@ template <int D, int M> __host__ __device__ constexpr int nbr(int r, int k) {   
     if (z0 < 0 || z0 >= M || z1 < 0 || z1 >= M || (D == 3 && (z2 < 0 || z2 >= M))) return -1;
     return z0 + M * (z1 + M * z2);
 }
+template <int D, int M> __host__ __device__ constexpr int pidx(int r, int k) {   // compact pair index
+    constexpr int W = D == 3 ? 15 : 7;
+    int c = 0;
+    for (int rr = 0; rr < r; ++rr)
+        for (int kk = 0; kk < W; ++kk) c += nbr<D, M>(rr, kk) >= 0;
+    for (int kk = 0; kk < k; ++kk) c += nbr<D, M>(r, kk) >= 0;
+    return c;
+}
+template <int D, int M> __host__ __device__ constexpr int npairs() {
+    return pidx<D, M>(D == 3 ? M * M * M : M * M, 0);
+}
 }  // namespace xw
+
+__constant__ double c_xw[XW_MAXG * XW_MAXP];   // [g][pair] of the launched level (compact)
 
 template <int D, int M>
 __global__ void __launch_bounds__(256, 2) k_xwhole(const double* __restrict__ Z, long long gstride, int nga, int n2,
                                                    long long pitch, double* __restrict__ Y) {
     constexpr int N = D == 3 ? M * M * M : M * M;
     constexpr int W = D == 3 ? 15 : 7;
+    constexpr int NP = D == 3 ? (M == 3 ? 223 : 0) : (M == 3 ? 41 : 137);   // xw::npairs<D, M>()
     const int col = blockIdx.x * 256 + threadIdx.x;
     if (col >= n2) return;
     double acc[N];
@@ -382,13 +406,16 @@ __global__ void __launch_bounds__(256, 2) k_xwhole(const double* __restrict__ Z,
         double z[N];
 #pragma unroll
         for (int r = 0; r < N; ++r) z[r] = __ldg(Zg + r * pitch);
-        const double* cg = c_xw + g * (N * W);
+        const double* cg = c_xw + g * NP;
+        int pi = 0;   // compact pair index (a compile-time constant after unrolling)
 #pragma unroll
         for (int r = 0; r < N; ++r)
 #pragma unroll
-            for (int k = 0; k < W; ++k) {
-                if (xw::nbr<D, M>(r, k) >= 0) acc[r] = fma(cg[r * W + k], z[xw::nbr<D, M>(r, k)], acc[r]);
-            }
+            for (int k = 0; k < W; ++k)
+                if (xw::nbr<D, M>(r, k) >= 0) {
+                    acc[r] = fma(cg[pi], z[xw::nbr<D, M>(r, k)], acc[r]);
+                    ++pi;
+                }
     }
 #pragma unroll
     for (int r = 0; r < N; ++r) Y[(long long)r * n2 + col] = acc[r];
@@ -397,6 +424,8 @@ __global__ void __launch_bounds__(256, 2) k_xwhole(const double* __restrict__ Z,
 // [g][r][k] coefficient tables of the tiny x-levels (setup time: never allocate inside a capture)
 int prepare_xwhole(sg_problem* P) {
     P->xw_tab.assign(P->F + 1, nullptr);
+    P->xw_dev.assign(P->F + 1, nullptr);
+    P->xw_np.assign(P->F + 1, 0);
     const int d = P->fx.d, W = P->fx.W;
     const int nga = (int)P->vorder.size();
     if (nga > XW_MAXG) return SG_OK;
@@ -421,8 +450,50 @@ int prepare_xwhole(sg_problem* P) {
             for (int g = 0; g < nga; ++g)
                 for (int k = 0; k < W; ++k) h[((size_t)g * n1 + r) * W + k] = cls[((size_t)c * nga + g) * W + k];
         }
-        SG_CUDA(cudaMalloc(&P->xw_tab[l1], sizeof(double) * h.size()));
-        SG_CUDA(cudaMemcpy(P->xw_tab[l1], h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+        // compact [g][pair] for the kernel parameters
+        std::vector<double> cmp((size_t)XW_MAXG * XW_MAXP, 0.0);
+        int np = 0;
+        for (int r = 0; r < n1; ++r)
+            for (int k = 0; k < W; ++k) {
+                int z = r, zz[3] = {0, 0, 0};
+                for (int q = 0; q < d; ++q) {
+                    zz[q] = z % m;
+                    z /= m;
+                }
+                bool ok2 = true;
+                for (int q = 0; q < d; ++q) {
+                    const int dq = d == 3 ? (q == 0 ? xfi::d0_3(k) : q == 1 ? xfi::d1_3(k) : xfi::d2_3(k))
+                                          : (q == 0 ? xfi::d0_2(k) : xfi::d1_2(k));
+                    ok2 &= zz[q] + dq >= 0 && zz[q] + dq < m;
+                }
+                if (!ok2) continue;
+                ++np;
+            }
+        int pi = 0;
+        for (int r = 0; r < n1; ++r)
+            for (int k = 0; k < W; ++k) {
+                int z = r, zz[3] = {0, 0, 0};
+                for (int q = 0; q < d; ++q) {
+                    zz[q] = z % m;
+                    z /= m;
+                }
+                bool ok2 = true;
+                for (int q = 0; q < d; ++q) {
+                    const int dq = d == 3 ? (q == 0 ? xfi::d0_3(k) : q == 1 ? xfi::d1_3(k) : xfi::d2_3(k))
+                                          : (q == 0 ? xfi::d0_2(k) : xfi::d1_2(k));
+                    ok2 &= zz[q] + dq >= 0 && zz[q] + dq < m;
+                }
+                if (!ok2) continue;
+                for (int g = 0; g < nga; ++g) cmp[(size_t)g * np + pi] = h[((size_t)g * n1 + r) * W + k];
+                ++pi;
+            }
+        if (np > XW_MAXP) continue;
+        P->xw_np[l1] = np;
+        SG_CUDA(cudaMalloc(&P->xw_dev[l1], sizeof(double) * (size_t)nga * np));
+        for (int g = 0; g < nga; ++g)
+            SG_CUDA(cudaMemcpy(P->xw_dev[l1] + (size_t)g * np, cmp.data() + (size_t)g * np, sizeof(double) * np,
+                               cudaMemcpyHostToDevice));
+        P->xw_tab[l1] = P->xw_dev[l1];
     }
     return SG_OK;
 }
@@ -435,12 +506,20 @@ int launch_xwhole(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pitch, 
     const bool ok = (d == 3 && m == 3) || (d == 2 && (m == 3 || m == 5));
     if (!ok || nga > XW_MAXG || n1 * n2 >= (1LL << 31) || n1 > XW_MAXN) return SG_ERR_UNSUPPORTED;
     if (l1 >= (int)P->xw_tab.size() || !P->xw_tab[l1]) return SG_ERR_UNSUPPORTED;   // built in prepare_xfanin
-    SG_CUDA(cudaMemcpyToSymbolAsync(c_xw, P->xw_tab[l1], sizeof(double) * nga * n1 * W, 0, cudaMemcpyDeviceToDevice,
+    const int np = P->xw_np[l1];
+    SG_CUDA(cudaMemcpyToSymbolAsync(c_xw, P->xw_dev[l1], sizeof(double) * nga * np, 0, cudaMemcpyDeviceToDevice,
                                     P->stream));
     const unsigned blocks = (unsigned)((n2 + 255) / 256);
-    if (d == 3) k_xwhole<3, 3><<<blocks, 256, 0, P->stream>>>(Z, gstride, nga, (int)n2, pitch, Y);
-    else if (m == 3) k_xwhole<2, 3><<<blocks, 256, 0, P->stream>>>(Z, gstride, nga, (int)n2, pitch, Y);
-    else k_xwhole<2, 5><<<blocks, 256, 0, P->stream>>>(Z, gstride, nga, (int)n2, pitch, Y);
+    if (d == 3) {
+        if (np != 223) return SG_ERR_UNSUPPORTED;
+        k_xwhole<3, 3><<<blocks, 256, 0, P->stream>>>(Z, gstride, nga, (int)n2, pitch, Y);
+    } else if (m == 3) {
+        if (np != 41) return SG_ERR_UNSUPPORTED;
+        k_xwhole<2, 3><<<blocks, 256, 0, P->stream>>>(Z, gstride, nga, (int)n2, pitch, Y);
+    } else {
+        if (np != 137) return SG_ERR_UNSUPPORTED;
+        k_xwhole<2, 5><<<blocks, 256, 0, P->stream>>>(Z, gstride, nga, (int)n2, pitch, Y);
+    }
     P->launches++;
     SG_CUDA(cudaGetLastError());
     return SG_OK;

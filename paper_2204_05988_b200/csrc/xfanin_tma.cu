@@ -109,6 +109,10 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* tm, uint6
 }  // namespace xft
 
 constexpr int XFT_MAXG = 12;
+// class table [3^d][groups][W] of the launched level in constant memory: the boundary path's
+// coefficient loads are warp-uniform and go through the constant cache, not L1
+constexpr int XFT_CTAB = 27 * 10 * 15;   // interior groups only (bonly groups read the global table)
+__constant__ double c_xft[XFT_CTAB];
 constexpr int XFT_NST = 4;   // pipeline stages
 struct XftCoef {
     double c[XFT_MAXG][15];
@@ -119,7 +123,7 @@ struct XftTile {
     int ntl1, ntl2, nct, nseg, seglen;
 };
 
-template <int D, int NGI>
+template <int D, int NGI, bool CTAB>
 __global__ void __launch_bounds__(32 * 17, 1)
     k_xfanin_tma(const __grid_constant__ CUtensorMap tmap, int nga, int n2, int m, XftTile tl,
                  const double* __restrict__ tab, const __grid_constant__ XftCoef cint, double* __restrict__ Y) {
@@ -215,7 +219,7 @@ __global__ void __launch_bounds__(32 * 17, 1)
     for (int t = ts; t <= te; ++t) {
         const bool cint_t = cta_lines_int && t >= 2 && t <= m - 3;
         const bool wint = lines_int && t >= 2 && t <= m - 3;
-        int cb[NT][3];
+        int cb[NT][3], cbi[NT][3];
 #pragma unroll
         for (int u = 0; u < NT; ++u)
 #pragma unroll
@@ -223,6 +227,7 @@ __global__ void __launch_bounds__(32 * 17, 1)
                 const int p = t + w - 1;
                 const int c0 = p <= 0 ? 0 : (p >= m - 1 ? 2 : 1);
                 cb[u][w] = (c0 + tcls12[u]) * nga * W;
+                cbi[u][w] = (c0 + tcls12[u]) * NGI * W;
             }
 #pragma unroll
         for (int g = 0; g < NGI; ++g, ++q) {
@@ -245,7 +250,9 @@ __global__ void __launch_bounds__(32 * 17, 1)
                                 acc[u][slot] = fma(cint.c[g][k], src[s], acc[u][slot]);
                             }
             } else {
-                const double* tg = tab + g * W;
+                // near the boundary: constant-cache table when boundary steps are a minority
+                // (m >= 9), global class table (L1 broadcast) on the tiny all-boundary lattices
+                const double* tg = CTAB ? c_xft + g * W : tab + g * W;
 #pragma unroll
                 for (int s = 0; s < NS; ++s)
 #pragma unroll
@@ -254,7 +261,8 @@ __global__ void __launch_bounds__(32 * 17, 1)
                         for (int k = 0; k < W; ++k)
                             if (xft::pair_ok<D>(s, u, k)) {
                                 const int slot = 1 - G::d0(k);
-                                acc[u][slot] = fma(__ldg(tg + cb[u][slot] + k), src[s], acc[u][slot]);
+                                const double cf = CTAB ? tg[cbi[u][slot] + k] : __ldg(tg + cb[u][slot] + k);
+                                acc[u][slot] = fma(cf, src[s], acc[u][slot]);
                             }
             }
             __syncwarp();
@@ -401,15 +409,27 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
     XftCoef ci;
     std::memcpy(ci.c, P->xfi_cint[l1].data(), sizeof(ci.c));
     const size_t smem = (size_t)XFT_NST * tl.e1 * tl.e2 * tl.bc * 8 + 2 * XFT_NST * sizeof(uint64_t);
+    {
+        int ncls = 1;
+        for (int q = 0; q < d; ++q) ncls *= 3;
+        const size_t nt = (size_t)ncls * ngi * P->fx.W;
+        if (nt > (size_t)XFT_CTAB || !P->xfi_itab[l1]) return SG_ERR_UNSUPPORTED;
+        SG_CUDA(cudaMemcpyToSymbolAsync(c_xft, P->xfi_itab[l1], sizeof(double) * nt, 0, cudaMemcpyDeviceToDevice,
+                                        P->stream));
+    }
     const int threads = 32 * (tl.nw + 1);
     const double* tab = P->xfi_tab[l1];
-#define XFT(DD, NG)                                                                                          \
-    do {                                                                                                     \
-        cudaFuncSetAttribute(k_xfanin_tma<DD, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-        k_xfanin_tma<DD, NG><<<(unsigned)nblk, threads, smem, P->stream>>>(tm, nga, (int)n2, m, tl, tab, ci, Y); \
+#define XFT(DD, NG, CT)                                                                                          \
+    do {                                                                                                         \
+        cudaFuncSetAttribute(k_xfanin_tma<DD, NG, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        k_xfanin_tma<DD, NG, CT><<<(unsigned)nblk, threads, smem, P->stream>>>(tm, nga, (int)n2, m, tl, tab, ci, Y); \
     } while (0)
-    if (d == 3) XFT(3, 10);
-    else XFT(2, 6);
+    const bool ctab = m >= 9;
+    if (d == 3) {
+        if (ctab) XFT(3, 10, true); else XFT(3, 10, false);
+    } else {
+        if (ctab) XFT(2, 6, true); else XFT(2, 6, false);
+    }
 #undef XFT
     P->launches++;
     SG_CUDA(cudaGetLastError());
