@@ -243,7 +243,9 @@ def main():
     achieved_gbs = (kt["bytes"] / 1e9) / (kt["ms"] / 1e3) if kt["ms"] > 0 else None
     roof = {"bound": "alu", "achieved": achieved_tf, "peak": fp64_peak_tflops, "unit": "TFLOP/s",
             "frac": (achieved_tf / fp64_peak_tflops) if achieved_tf else None, "traffic": None,
-            "kernel": "strip-operator apply per component grid (k_vfan_st + k_xgat_st, 2-pass stencil kernels)",
+            "kernel": ("strip-operator apply per component grid: pass 1 along v (k_vfan_st on 3D v-lattices, "
+                       "k_vmom shifted moments on 2D) + pass 2 along x (k_xfanin_tma TMA-pipelined line sweep, "
+                       "k_xwhole on level-1/2 x-lattices); CUDA events around every apply"),
             "peak_source": "derived fp64: 148 SM x 64 FMA/clk x 2 x sm_max_mhz (DESIGN.md sec. 5)",
             "algorithmic_flops_per_launch": kt["flops"] / max(kt["launches"], 1),
             "hbm_view": {"achieved_gbs": achieved_gbs, "peak_gbs": hbm,
@@ -267,6 +269,7 @@ def main():
            "time_steps_per_s": args.steps * world / (ms_max / 1e3),
            "gpu_launches": st["launches"],
            "applies": st["applies"], "outer_iters": st["outer_iters"], "inner_iters": st["inner_iters"],
+           "outer_mr_switches": st.get("outer_mr_switches"),
            "setup_s": t_setup, "roofline": roof, "clocks": clocks, "e2e": e2e}
     if rank == 0 and world == 1 and not args.no_cpu:
         try:

@@ -178,6 +178,10 @@ int sg_step(sg_problem* P, int j0, int nsteps, double* trace, double rtol, doubl
 int sg_stats(const sg_problem* P, int64_t* n_applies, int64_t* dof_applied, int64_t* launches,
              int64_t* outer_iters, int64_t* inner_iters);
 int sg_reset_stats(sg_problem* P);
+/* number of strip solves (since the last reset) in which the outer Richardson
+ * iteration switched to residual-minimising step lengths because the update
+ * norm grew (safeguard, reading R13); SG_OUTER=1 disables it */
+int sg_outer_switches(const sg_problem* P, int64_t* switches);
 /* when on, CUDA events bracket every launch of the strip-operator kernels;
  * sg_kernel_time returns their summed device time (ms), launch count and
  * algorithmic bytes (read X + write Y + factor matrices) */

@@ -83,6 +83,7 @@ def load_library():
         "sg_solve_strip": (I, [P, P, P, D, D, I, pI, pD]),
         "sg_step": (I, [P, I, I, P, D, D]),
         "sg_stats": (I, [P, pI64, pI64, pI64, pI64, pI64]),
+        "sg_outer_switches": (I, [P, pI64]),
         "sg_reset_stats": (I, [P]),
         "sg_set_timing": (I, [P, I]),
         "sg_kernel_time": (I, [P, pD, pI64, pD, pD]),
@@ -300,7 +301,10 @@ class Problem:
     def stats(self):
         v = [C.c_int64() for _ in range(5)]
         _check(self.lib.sg_stats(self.h, *[C.byref(x) for x in v]))
-        return dict(zip(["applies", "dof_applied", "launches", "outer_iters", "inner_iters"], [x.value for x in v]))
+        sw = C.c_int64()
+        _check(self.lib.sg_outer_switches(self.h, C.byref(sw)))
+        return dict(zip(["applies", "dof_applied", "launches", "outer_iters", "inner_iters", "outer_mr_switches"],
+                        [x.value for x in v] + [sw.value]))
 
     def reset_stats(self):
         _check(self.lib.sg_reset_stats(self.h))

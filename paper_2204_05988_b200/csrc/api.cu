@@ -70,6 +70,7 @@ extern "C" int sg_create(const sg_config* cfg, void* stream, sg_problem** out) {
     P->use_xfi_tma = getenv("SG_NO_TMA") == nullptr;
     P->use_xwhole = getenv("SG_NO_XWHOLE") == nullptr;
     P->use_cross_batched = getenv("SG_NO_CROSS_BATCH") == nullptr;
+    P->outer_mode = getenv("SG_OUTER") ? atoi(getenv("SG_OUTER")) : 0;
     // moment pass 1: faster than the stored-stencil kernel for d = 2 v-lattices, slower for d = 3
     // (round-1 measurements, profiles/README.md); SG_VMOM forces it on, SG_NO_VMOM off
     P->use_vmom = getenv("SG_NO_VMOM") == nullptr && (getenv("SG_VMOM") != nullptr || cfg->d == 2);
@@ -193,10 +194,10 @@ extern "C" int sg_assemble_factors(sg_problem* P) {
     SG_CUDA(cudaMemset(P->scal, 0, sizeof(double) * 10 * (MAX_SEG + 1)));
     SG_CUDA(cudaMallocHost(&P->hscal, sizeof(double) * 10 * (MAX_SEG + 1)));
     const int64_t nF = std::max(P->fx.lev[F].n, P->fv.lev[F].n) + 16;
-    const int64_t sizes[15] = {Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na, Na + Nc, Na + Nc, Na,
-                               std::max(Na, 4 * nF), Na, Na, Na + Nc, Na + Nc};
-    P->vec.assign(15, nullptr);
-    for (int i = 0; i < 15; ++i) SG_CUDA(cudaMalloc(&P->vec[i], sizeof(double) * sizes[i]));
+    const int64_t sizes[16] = {Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na, Na + Nc, Na + Nc, Na,
+                               std::max(Na, 4 * nF), Na, Na, Na + Nc, Na + Nc, Na};
+    P->vec.assign(16, nullptr);
+    for (int i = 0; i < 16; ++i) SG_CUDA(cudaMalloc(&P->vec[i], sizeof(double) * sizes[i]));
     P->use_precond = getenv("SG_NO_PRECOND") == nullptr;
     SG_TRY(build_block_jacobi(P));
     SG_CUDA(cudaMalloc(&P->trace_dev, sizeof(double) * set_size(P, SG_SET_ACTIVE, 1)));
@@ -482,6 +483,7 @@ extern "C" int sg_stats(const sg_problem* P, int64_t* n_applies, int64_t* dof_ap
 extern "C" int sg_reset_stats(sg_problem* P) {
     CHECK_ARG(P, "null handle");
     P->n_applies = P->dof_applied = P->launches = P->outer_iters = P->inner_iters = 0;
+    P->mr_switches = 0;
     SG_CUDA(cudaStreamSynchronize(P->stream));
     for (auto& pr : P->ev_pairs) {
         cudaEventDestroy(pr.first);
@@ -513,5 +515,11 @@ extern "C" int sg_kernel_time(sg_problem* P, double* ms, int64_t* launches, doub
     if (launches) *launches = P->kern_launches;
     if (alg_bytes) *alg_bytes = P->kern_bytes;
     if (alg_flops) *alg_flops = P->kern_flops;
+    return SG_OK;
+}
+
+extern "C" int sg_outer_switches(const sg_problem* P, int64_t* switches) {
+    CHECK_ARG(P && switches, "null argument");
+    *switches = P->mr_switches;
     return SG_OK;
 }

@@ -238,7 +238,10 @@ struct sg_problem {
     double* cross_q = nullptr;     // batched cross-grid lower part: stage-0 fan-outs of all v-groups
     double* cross_h = nullptr;     //   and the Horner results per target and group (even pitch)
     bool cross_batched_tried = false;
+    int64_t cross_q_n = 0, cross_h_n = 0;
     bool use_cross_batched = true; // SG_NO_CROSS_BATCH disables
+    int outer_mode = 0;            // 0 Richardson + minimal-residual safeguard, 1 plain Richardson, 2 MR always
+    int64_t mr_switches = 0;
     bool use_vmom = true;          // moment pass 1 (SG_NO_VMOM disables)
     std::vector<int> vm_ok;        // per v-level: moment tables verified
     std::vector<double*> vm_tab;   // per v-level: [3^d][10][W] shifted-moment class tables

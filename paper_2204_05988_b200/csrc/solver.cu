@@ -542,8 +542,17 @@ static int cross_lower_batched(sg_problem* P, const double* X, double* Y) {
         ho[p + 1] = ho[p] + (int64_t)nga * n1(p) * pit(L - p);
     }
     if (!P->cross_batched_tried) {
-        // first use: allocate outside any stream capture (apply_cross calls us uncaptured first)
+        // first use: allocate outside any stream capture (apply_cross calls us uncaptured first);
+        // sized for the lower part (v-groups) and the batched upper part (x-groups)
         P->cross_batched_tried = true;
+        const int nxg = (int)P->xgroups.size();
+        int64_t qu = 0, hu = 0;
+        for (int pp = 2; pp <= ng; ++pp) qu += (int64_t)nxg * n1(pp) * n2(L - pp);
+        for (int p = 1; p <= ng - 1; ++p) hu += (int64_t)nxg * n1(p) * n2(L - p);
+        P->cross_q_n = std::max<int64_t>(qo[ng + 1], qu);
+        P->cross_h_n = std::max<int64_t>(ho[ng + 1], hu);
+        qo[ng + 1] = P->cross_q_n;
+        ho[ng + 1] = P->cross_h_n;
         if (cudaMalloc(&P->cross_q, sizeof(double) * qo[ng + 1]) != cudaSuccess ||
             cudaMalloc(&P->cross_h, sizeof(double) * ho[ng + 1]) != cudaSuccess) {
             cudaGetLastError();
@@ -622,6 +631,102 @@ static int cross_lower_batched(sg_problem* P, const double* X, double* Y) {
             if (rc == SG_ERR_UNSUPPORTED) set_error("apply_cross: batched gather unsupported after setup");
             return rc == SG_ERR_UNSUPPORTED ? SG_ERR_STATE : rc;
         }
+    }
+    return SG_OK;
+}
+
+
+// Batched upper part of the cross-grid apply (targets p < sources p'), S = 1 box lattices:
+// all x-groups fanned out once per source (k_xfan_st, every row), per group the restriction
+// chains in x and the Horner prolongation in v (last stage -> Hu[p][a]), then ONE v-gather
+// over all x-groups per target (k_vgat_st, one read-modify-write of Y instead of one per group).
+static int cross_upper_batched(sg_problem* P, const double* X, double* Y) {
+    if (!P->use_cross_batched || P->S != 1 || P->fx.kind != SG_MESH_BOX || P->fv.kind != SG_MESH_BOX || P->fx.d < 2 ||
+        !P->cross_q || !P->cross_h)
+        return SG_ERR_UNSUPPORTED;
+    const auto& A = P->active;
+    const int ng = (int)A.size();
+    const int L = P->cfg.L;
+    const int nxg = (int)P->xgroups.size();
+    const int Wx = P->fx.W;
+    if (ng < 2) return SG_OK;
+    if (nxg > MAXG || nxg > MAX_ENTRIES) return SG_ERR_UNSUPPORTED;
+    for (int a = 0; a < nxg; ++a)
+        for (int l = 1; l <= P->F; ++l)
+            if (P->xgroups[a].comb[l].size() != 1) return SG_ERR_UNSUPPORTED;
+    auto n1 = [&](int l) { return P->fx.lev[l].n; };
+    auto n2 = [&](int l) { return P->fv.lev[l].n; };
+    std::vector<int64_t> qo(ng + 2, 0), ho(ng + 2, 0);
+    for (int pp = 2; pp <= ng; ++pp) qo[pp + 1] = qo[pp] + (int64_t)nxg * n1(pp) * n2(L - pp);
+    qo[ng + 1] = std::max(qo[ng + 1], qo[ng]);
+    for (int p = 1; p <= ng - 1; ++p) ho[p + 1] = ho[p] + (int64_t)nxg * n1(p) * n2(L - p);
+    if (qo[ng + 1] > P->cross_q_n || ho[ng] > P->cross_h_n) return SG_ERR_UNSUPPORTED;
+    auto Q0 = [&](int pp, int a) { return P->cross_q + qo[pp] + (int64_t)a * n1(pp) * n2(L - pp); };
+    auto H = [&](int p, int a) { return P->cross_h + ho[p] + (int64_t)a * n1(p) * n2(L - p); };
+    // 1. x fan-out of every x-group at every source pp >= 2 (all rows: the chains mix rows)
+    for (int pp = 2; pp <= ng; ++pp) {
+        const Level& Lx = P->fx.lev[pp];
+        XfanParams fp;
+        fp.ng = fp.ng_int = nxg;
+        for (int a = 0; a < nxg; ++a) {
+            const int sp = P->xgroups[a].spec;
+            fp.cst[a] = Lx.fst[sp];
+            fp.ctab[a] = Lx.fcls.size() > (size_t)sp ? Lx.fcls[sp] : nullptr;
+            fp.out[a] = Q0(pp, a);
+        }
+        SG_TRY(launch_xfan_st(P, P->fx.d, 1, n1(pp), n2(L - pp), Lx.so, Lx.m, Lx.bflag, fp, X + A[pp - 1].off1));
+    }
+    // 2./3. per group: restriction chains in x, Horner prolongation in v
+    std::vector<std::vector<int64_t>> qoff(ng);
+    for (int a = 0; a < nxg; ++a) {
+        int64_t pos = 0;
+        for (int pp = 2; pp <= ng; ++pp) {
+            const int lv = L - pp;
+            qoff[pp - 1].assign(pp, 0);
+            for (int k = 1; k <= pp - 1; ++k) {   // k: x-level pp-k
+                qoff[pp - 1][k] = pos;
+                pos += n1(pp - k) * n2(lv);
+            }
+        }
+        if ((size_t)pos > P->wsZ_n) {
+            set_error("apply_cross: chain workspace too small (upper)");
+            return SG_ERR_STATE;
+        }
+        auto Q = [&](int pp, int k) -> double* { return k == 0 ? Q0(pp, a) : P->wsZ + qoff[pp - 1][k]; };
+        for (int k = 1; k <= ng - 1; ++k) {
+            std::vector<Job> jobs;
+            for (int pp = k + 1; pp <= ng; ++pp) {
+                const int lv = L - pp, lf = pp - k + 1, lc = pp - k;
+                jobs.push_back({Q(pp, k - 1), nullptr, Q(pp, k), P->fx.lev[lf].rcols, P->fx.lev[lf].rvals, n1(lf), n2(lv),
+                                n1(lc), 1.0, 1, 0, Wx, 0});
+            }
+            SG_TRY(launch_jobs(P, jobs));
+        }
+        double* hb[2] = {P->wsH, P->wsH + set_size(P, SG_SET_ACTIVE, 1)};
+        for (int q = 1; q <= ng - 1; ++q) {
+            std::vector<Job> jobs;
+            const int lvn = L - ng + q;
+            for (int p = 1; p <= ng - q; ++p) {
+                const double* in = q == 1 ? Q(ng, ng - p) : hb[(q - 1) & 1] + A[p - 1].off1;
+                const int pp = ng - q;
+                const double* add = pp > p ? Q(pp, pp - p) : nullptr;
+                double* out = (q == ng - p) ? H(p, a) : hb[q & 1] + A[p - 1].off1;
+                jobs.push_back({in, add, out, P->fv.lev[lvn].pcols, P->fv.lev[lvn].pvals, n1(p), n2(lvn - 1), n2(lvn), 1.0,
+                                1, 1, 2, 0});
+            }
+            SG_TRY(launch_jobs(P, jobs));
+        }
+    }
+    // 4. one v-gather over all x-groups per target
+    for (int p = 1; p <= ng - 1; ++p) {
+        const int lvt = L - p;
+        XgatParams ep;
+        ep.ne = 0;
+        for (int a = 0; a < nxg; ++a) {
+            const auto& ce = P->xgroups[a].comb[lvt][0];
+            ep.e[ep.ne++] = {H(p, a), ce.st, ce.s_out, ce.s_in, 0, 1.0};
+        }
+        SG_TRY(launch_vgat_st(P, P->fv.d, 1, n1(p), n2(lvt), P->fv.lev[lvt].so, ep, Y + A[p - 1].off1, 1.0));
     }
     return SG_OK;
 }
@@ -743,7 +848,13 @@ static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in
         }
     }
     // ---------------- upper part (targets p < sources p')
-    if (ng >= 2) {
+    bool upper_done = false;
+    if (!mass && lower_done) {
+        int rc = cross_upper_batched(P, X, Y);
+        if (rc == SG_OK) upper_done = true;
+        else if (rc != SG_ERR_UNSUPPORTED) return rc;
+    }
+    if (ng >= 2 && !upper_done) {
         const int nxg = mass ? 1 : (int)P->xgroups.size();
         for (int a = 0; a < nxg; ++a) {
             const int xspec = mass ? P->mass_x : P->xgroups[a].spec;
@@ -871,9 +982,14 @@ constexpr int NSC = 10;
 // partial[blk*K + j] = sum over the block's chunk of a_j * b_j
 template <int K>
 __global__ void k_seg_dot(SegTab t, const double* a0, const double* b0, const double* a1, const double* b1,
-                          double* partial, const double* a2 = nullptr, const double* b2 = nullptr) {
+                          double* partial, const double* a2 = nullptr, const double* b2 = nullptr,
+                          const double* scal = nullptr) {
     __shared__ double sh[K][8];
     const int g = seg_of(t, blockIdx.x);
+    if (scal && scal[g * NSC + 5] != 0.0) {   // converged grid: its scalars are frozen
+        if (threadIdx.x < K) partial[(int64_t)blockIdx.x * K + threadIdx.x] = 0.0;
+        return;
+    }
     const int64_t lo = t.off[g] + (int64_t)(blockIdx.x - t.blk[g]) * SEG_CHUNK;
     const int64_t hi = min(lo + SEG_CHUNK, t.off[g + 1]);
     double s[K];
@@ -983,6 +1099,10 @@ __global__ void k_bicg_xr(SegTab tb, const double* scal, double* x, double* r, c
     const int g = seg_of(tb, blockIdx.x);
     const double* sc = scal + g * NSC;
     const bool active = sc[5] == 0.0;
+    if (!active) {   // converged grid: frozen, no traffic
+        if (threadIdx.x < 2) partial[(int64_t)blockIdx.x * 2 + threadIdx.x] = 0.0;
+        return;
+    }
     const double al = sc[1], om = sc[2];
     const int64_t lo = tb.off[g] + (int64_t)(blockIdx.x - tb.blk[g]) * SEG_CHUNK;
     const int64_t hi = min(lo + SEG_CHUNK, tb.off[g + 1]);
@@ -1163,7 +1283,7 @@ static int bicgstab(sg_problem* P, const std::vector<const Grid*>& gr, const dou
         }
         for (size_t i = 0; i < gr.size(); ++i)
             if (!conv[i]) SG_TRY(apply_diag(P, *gr[i], pa + offs[i], v + offs[i]));
-        k_seg_dot<1><<<nblk, 256, 0, P->stream>>>(t, r0, v, nullptr, nullptr, P->red);
+        k_seg_dot<1><<<nblk, 256, 0, P->stream>>>(t, r0, v, nullptr, nullptr, P->red, nullptr, nullptr, P->scal);
         k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 1, P->red, P->scal, 6, 6, 1, tol2);
         k_bicg_s<<<nblk, 256, 0, P->stream>>>(t, P->scal, r, v, s);
         const double* sa = s;
@@ -1174,7 +1294,7 @@ static int bicgstab(sg_problem* P, const std::vector<const Grid*>& gr, const dou
         }
         for (size_t i = 0; i < gr.size(); ++i)
             if (!conv[i]) SG_TRY(apply_diag(P, *gr[i], sa + offs[i], tt + offs[i]));
-        k_seg_dot<3><<<nblk, 256, 0, P->stream>>>(t, tt, s, tt, tt, P->red, s, s);
+        k_seg_dot<3><<<nblk, 256, 0, P->stream>>>(t, tt, s, tt, tt, P->red, s, s, P->scal);
         k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 3, P->red, P->scal, 7, 8, 2, tol2);
         k_bicg_xr<<<nblk, 256, 0, P->stream>>>(t, P->scal, x, r, pa, sa, s, tt, r0, P->red);
         k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 2, P->red, P->scal, 0, 4, 3, tol2);
@@ -1246,11 +1366,21 @@ int solve_strip(sg_problem* P, const double* b, double* u, double rtol, double i
     Mt[0] = P->cfg.tau;
     if (S == 2) Mt[3] = P->cfg.tau / 3.0;
     int it = 0;
-    double nd = 0.0, nu_est = 0.0;
+    double nd = 0.0, nu_est = 0.0, nd_prev = 0.0;
+    // Outer iteration: the paper's Richardson u <- u - P^{-1} r (l.540-546).  Safeguard: when the
+    // update norm grows (the combination preconditioner is not a contraction, e.g. configs[2]
+    // at L = 12) the step length switches to the residual-minimising omega_k = (r, A du)/(A du, A du)
+    // for the rest of the solve (same one cross-grid apply per iteration, residual updated
+    // recursively); P->outer_mode: 0 paper + safeguard, 1 paper only, 2 minimal residual always.
+    bool mr = P->outer_mode == 2;
+    bool have_r = false;
+    double* w = P->vec[15];   // A du (minimal-residual steps)
     for (it = 1; it <= max_iter; ++it) {
         P->outer_iters++;
-        SG_TRY(apply_cross(P, nullptr, nullptr, S, S, u, r));                 // r = A u
-        SG_TRY(launch_axpby(P, Na, -1.0, b, 1.0, r));                        // r -= b
+        if (!have_r) {
+            SG_TRY(apply_cross(P, nullptr, nullptr, S, S, u, r));                 // r = A u
+            SG_TRY(launch_axpby(P, Na, -1.0, b, 1.0, r));                        // r -= b
+        }
         SG_TRY(launch_copy(P, Na, r, rhs));
         for (size_t c = 0; c < P->coarse.size(); ++c) {                       // (Id x E^T x Id) r, l.552
             const Grid& cg = P->coarse[c];
@@ -1263,10 +1393,19 @@ int solve_strip(sg_problem* P, const double* b, double* u, double rtol, double i
         }
         SG_TRY(bicgstab(P, gr, rhs, dhat, inner_rtol, 500));
         SG_TRY(combine(P, S, dhat, dhat + Na, du));
-        SG_TRY(launch_axpby(P, Na, -1.0, du, 1.0, u));
         int err = SG_OK;
+        double omega = 1.0;
+        if (mr) {
+            SG_TRY(apply_cross(P, nullptr, nullptr, S, S, du, w));                // w = A du
+            const double rw = host_dot(P, Na, r, w, &err), ww = host_dot(P, Na, w, w, &err);
+            if (err) return err;
+            omega = (ww > 0.0 && std::isfinite(rw / ww)) ? rw / ww : 1.0;
+            SG_TRY(launch_axpby(P, Na, -omega, w, 1.0, r));                     // r <- r - omega A du
+            have_r = true;
+        }
+        SG_TRY(launch_axpby(P, Na, -omega, du, 1.0, u));
         SG_TRY(apply_cross(P, nullptr, Mt, S, S, du, Mw));
-        double nd2 = host_dot(P, Na, du, Mw, &err);
+        double nd2 = host_dot(P, Na, du, Mw, &err) * omega * omega;
         nd = std::sqrt(std::max(nd2, 0.0));
         // ||u|| only when the test can pass (it changes little once |du| is small)
         if (it == 1 || nd <= 4.0 * rtol * nu_est) {
@@ -1277,13 +1416,18 @@ int solve_strip(sg_problem* P, const double* b, double* u, double rtol, double i
         if (err) return err;
         double nu = nu_est;
         double nu2 = nu * nu;
-        if (P->verbose) fprintf(stderr, "[sg] richardson it %d |du| %.3e |u| %.3e inner %lld\n", it, nd, nu,
-                                (long long)P->inner_iters);
+        if (P->verbose) fprintf(stderr, "[sg] richardson it %d |du| %.3e |u| %.3e omega %.3f inner %lld\n", it, nd, nu,
+                                omega, (long long)P->inner_iters);
         if (!std::isfinite(nd2) || !std::isfinite(nu2)) {
             set_error("solve_strip: non-finite update (inner solver breakdown)");
             return SG_ERR_STATE;
         }
         if (nd <= rtol * nu || nd == 0.0) break;
+        if (!mr && P->outer_mode == 0 && it >= 2 && nd > nd_prev) {
+            mr = true;   // safeguard engaged; r is recomputed from u at the next iteration top
+            P->mr_switches++;
+        }
+        nd_prev = nd;
     }
     if (iters) *iters = std::min(it, max_iter);
     if (last) *last = nd;

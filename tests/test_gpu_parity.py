@@ -226,6 +226,28 @@ def test_solve_strip(name):
         assert relmax(f_gpu, f_ref) <= 1e-9, (s, it, git)
 
 
+@pytest.mark.parametrize("name", ["c2_4d_stream", "c4_6d_stream", "c1_2d_rot"])
+def test_solve_strip_minimal_residual_steps(name, monkeypatch):
+    """SG_OUTER=2 (residual-minimising step lengths from the first iteration, the safeguard's
+    mode): the same converged strip solution as the oracle's plain Richardson."""
+    from oracle.sgrid import SGProblem
+    from paper_2204_05988_b200 import Problem
+    monkeypatch.setenv("SG_OUTER", "2")
+    cfg = get_config(name, L=SMALL[name])
+    g, o = Problem(cfg), SGProblem(cfg)
+    tr0 = o.interp_u0()
+    b = o.rhs(1, tr0)
+    U, it, _ = o.solve_strip(b, rtol=1e-13)
+    ut = torch.zeros(g.set_size(SET_ACTIVE, o.S), dtype=torch.float64, device="cuda")
+    git, _ = g.sg_solve_strip(from_blocks(g, b), ut, rtol=1e-13, inner_rtol=1e-13, max_iter=200)
+    assert git < 200
+    G = to_blocks(g, ut)
+    for s in range(o.S):
+        f_ref = _full(o, {l: U[l][s:s + 1] for l in o.active})
+        f_gpu = _full(o, {l: G[l][s:s + 1] for l in o.active})
+        assert relmax(f_gpu, f_ref) <= 1e-9, (s, it, git)
+
+
 @pytest.mark.parametrize("name", CONFIG_ORDER)
 def test_step_matches_oracle(name):
     g, o = pair(name)

@@ -1,5 +1,5 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "apply_strip or cross_grid" 2>&1 | tail -5 > gpurun_out/t_apply.log
-for c in c4_6d_stream c2_4d_stream; do
-timeout 300 python tools/apply_bench.py --config $c --reps 3 --prof > gpurun_out/abp_$c.log 2>&1
-done
-cat gpurun_out/t_apply.log
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -5 > gpurun_out/t_all.log
+SG_VERBOSE=1 PRE=1 IRTS=1e-2 timeout 900 python tools/solver_experiment.py c2_4d_stream:12 > gpurun_out/solver_c2_12.log 2> gpurun_out/solver_c2_12.err
+SG_OUTER=2 PRE=1 IRTS=1e-2 timeout 900 python tools/solver_experiment.py c2_4d_stream:12 c4_6d_stream:8 > gpurun_out/solver_mr.log 2>&1
+PRE=1 IRTS=1e-2 timeout 900 python tools/solver_experiment.py c4_6d_stream:8 > gpurun_out/solver_c4.log 2>&1
+cat gpurun_out/t_all.log
