@@ -9,7 +9,12 @@ agg = defaultdict(lambda: [0, 0.0]); tot = 0.0
 for r in rows[start + 1:]:
     if len(r) <= vi: continue
     k = r[ni].split("(")[0]
-    v = float(r[vi].replace(",", ""))
+    try:
+        v = float(r[vi].replace(",", ""))
+    except ValueError:
+        continue
+    if v != v:   # nan: the launch that was cut off when ncu stopped
+        continue
     agg[k][0] += 1; agg[k][1] += v; tot += v
 print(f"launches {sum(a[0] for a in agg.values())}, device time {tot/1e6:.2f} ms (serialised, cold-cache)")
 for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
