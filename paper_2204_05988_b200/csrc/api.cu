@@ -71,6 +71,9 @@ extern "C" int sg_create(const sg_config* cfg, void* stream, sg_problem** out) {
     P->use_xwhole = getenv("SG_NO_XWHOLE") == nullptr;
     P->use_cross_batched = getenv("SG_NO_CROSS_BATCH") == nullptr;
     P->outer_mode = getenv("SG_OUTER") ? atoi(getenv("SG_OUTER")) : 0;
+    // k-outer pass-1 kernel: more rows per coefficient load but register-starved; measured slower
+    // than k_vfan_st on both 3D (1.35-1.86 vs 0.85 ms on grid (4,4)) in round 1: opt-in
+    P->use_vfan_k = getenv("SG_VFANK") != nullptr;
     // moment pass 1: faster than the stored-stencil kernel for d = 2 v-lattices, slower for d = 3
     // (round-1 measurements, profiles/README.md); SG_VMOM forces it on, SG_NO_VMOM off
     P->use_vmom = getenv("SG_NO_VMOM") == nullptr && (getenv("SG_VMOM") != nullptr || cfg->d == 2);

@@ -315,6 +315,121 @@ __global__ void __launch_bounds__(VF_TC * VF_RL, 2) k_vfan_st(int64_t nrows, int
     }
 }
 
+// Pass 1, k-outer variant: each thread owns VK rows of one column; for every stencil slot k
+// the VK X values are loaded once and every group's coefficient (one shared-memory load)
+// feeds VK FMAs, halving the coefficient loads per output of k_vfan_st.  Interior groups
+// first (accumulators acc[g][r] for g < ng_int), boundary-only groups in a second sweep
+// on blocks that contain an x-boundary row.
+template <int D, int NGI, int VK>
+__global__ void __launch_bounds__(VF_TC * VF_RL, 2) k_vfan_k(int64_t nrows, int64_t n1, int64_t n2, StencilOff so,
+                                                             const uint8_t* __restrict__ xflag, VfanParams vp,
+                                                             const double* __restrict__ X, int64_t rows_per_block,
+                                                             int64_t opitch) {
+    constexpr int W = stc::Bands<D>::W;
+    extern __shared__ double sm[];
+    __shared__ int soff[16];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int a = blockIdx.x * VF_TC + tx;
+    const bool aval = a < n2;
+    const int tot = vp.ng * W * VF_TC;
+    for (int idx = ty * VF_TC + tx; idx < tot; idx += VF_TC * VF_RL) {
+        const int g = idx / (W * VF_TC), rem = idx - g * W * VF_TC, k = rem / VF_TC, c = rem - k * VF_TC;
+        const int ac = blockIdx.x * VF_TC + c;
+        sm[idx] = ac < n2 ? __ldg(vp.vst[g] + (int64_t)k * n2 + ac) : 0.0;
+    }
+    if (ty == 0 && tx < W) soff[tx] = (int)so.off[tx];
+    __syncthreads();
+    const double* xa = X + a;
+    const int64_t rb = blockIdx.y * rows_per_block;
+    const int64_t re = min(nrows, rb + rows_per_block);
+    for (int64_t r0 = rb + ty * VK; r0 < re; r0 += VF_RL * VK) {
+        bool anyb = false;
+#pragma unroll
+        for (int r = 0; r < VK; ++r)
+            if (r0 + r < re) anyb |= xflag[(r0 + r) % n1] != 0;
+        const int nr = (int)min((int64_t)VK, re - r0);
+        const double* xr = xa + r0 * n2;
+        double acc[NGI][VK];
+#pragma unroll
+        for (int g = 0; g < NGI; ++g)
+#pragma unroll
+            for (int r = 0; r < VK; ++r) acc[g][r] = 0.0;
+#pragma unroll 1
+        for (int k = 0; k < W; ++k) {
+            const int o = soff[k];
+            const bool ok = aval && a + o >= 0 && a + o < n2;   // absent neighbours have zero coefficients
+            double xv[VK];
+#pragma unroll
+            for (int r = 0; r < VK; ++r) xv[r] = (ok && r < nr) ? __ldg(xr + r * n2 + o) : 0.0;
+            const double* cp = sm + k * VF_TC + tx;
+#pragma unroll
+            for (int g = 0; g < NGI; ++g) {
+                const double c = cp[g * W * VF_TC];
+#pragma unroll
+                for (int r = 0; r < VK; ++r) acc[g][r] = fma(c, xv[r], acc[g][r]);
+            }
+        }
+        if (aval) {
+#pragma unroll
+            for (int g = 0; g < NGI; ++g) {
+                double* op = vp.out[g] + a;
+#pragma unroll
+                for (int r = 0; r < VK; ++r)
+                    if (r < nr) op[(r0 + r) * opitch] = acc[g][r];
+            }
+        }
+        if (anyb) {
+            for (int g = NGI; g < vp.ng; ++g) {
+                double ab[VK];
+#pragma unroll
+                for (int r = 0; r < VK; ++r) ab[r] = 0.0;
+#pragma unroll 1
+                for (int k = 0; k < W; ++k) {
+                    const int o = soff[k];
+                    const bool ok = aval && a + o >= 0 && a + o < n2;
+                    const double c = sm[(g * W + k) * VF_TC + tx];
+#pragma unroll
+                    for (int r = 0; r < VK; ++r)
+                        ab[r] = fma(c, (ok && r < nr) ? __ldg(xr + r * n2 + o) : 0.0, ab[r]);
+                }
+                if (aval) {
+                    double* op = vp.out[g] + a;
+#pragma unroll
+                    for (int r = 0; r < VK; ++r)
+                        if (r < nr) op[(r0 + r) * opitch] = ab[r];
+                }
+            }
+        }
+    }
+}
+
+int launch_vfan_k(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, const uint8_t* xflag,
+                  const VfanParams& vp, const double* X, int64_t opitch) {
+    if (opitch <= 0) opitch = n2;
+    const int W = (1 << (d + 1)) - 1;
+    const int64_t nrows = (int64_t)S * n1;
+    const int64_t ctiles = (n2 + VF_TC - 1) / VF_TC;
+    int64_t rchunks = std::max<int64_t>(1, (148 * 6 + ctiles - 1) / ctiles);
+    rchunks = std::min<int64_t>(rchunks, (nrows + 31) / 32);
+    rchunks = std::max<int64_t>(rchunks, 1);
+    const int64_t rpb = (nrows + rchunks - 1) / rchunks;
+    const size_t smem = sizeof(double) * vp.ng * W * VF_TC;
+    dim3 grid((unsigned)ctiles, (unsigned)rchunks), block(VF_TC, VF_RL);
+#define VK_L(DD, NG, R)                                                                                      \
+    do {                                                                                                     \
+        cudaFuncSetAttribute(k_vfan_k<DD, NG, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+        k_vfan_k<DD, NG, R><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch); \
+    } while (0)
+    if (n1 * n2 >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
+    if (d == 3 && vp.ng_int == 10) VK_L(3, 10, 4);
+    else if (d == 2 && vp.ng_int == 6) VK_L(2, 6, 4);
+    else return SG_ERR_UNSUPPORTED;
+#undef VK_L
+    P->launches++;
+    SG_CUDA(cudaGetLastError());
+    return SG_OK;
+}
+
 // Pass 2 (x side): Y[s][i][a] = beta*Y + sum_e [s_out(e)=s] sum_k Cst_e[k][i] Z_e[s_in][i + off_k][a].
 // Block = 8 warps x T consecutive target rows (32 rows); warp lanes = columns,
 // CPT columns per lane.  The block's coefficients (chunk of entries) are staged

@@ -243,6 +243,7 @@ struct sg_problem {
     int outer_mode = 0;            // 0 Richardson + minimal-residual safeguard, 1 plain Richardson, 2 MR always
     int64_t mr_switches = 0;
     bool use_vmom = true;          // moment pass 1 (SG_NO_VMOM disables)
+    bool use_vfan_k = true;        // k-outer pass-1 kernel (SG_NO_VFANK disables)
     std::vector<int> vm_ok;        // per v-level: moment tables verified
     std::vector<double*> vm_tab;   // per v-level: [3^d][10][W] shifted-moment class tables
     std::vector<std::vector<double>> vm_int;   // per v-level: interior class [10][15]
@@ -281,6 +282,8 @@ int launch_ell_to_stencil(sg_problem* P, int64_t n, int W, const int32_t* cols, 
                           const StencilOff& so, double* out);
 int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, const uint8_t* xflag,
                    const VfanParams& vp, const double* X, int64_t opitch = 0);
+int launch_vfan_k(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, const uint8_t* xflag,
+                  const VfanParams& vp, const double* X, int64_t opitch = 0);
 int launch_xgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
                    const uint8_t* xflag, const XgatParams& ep, double* Y, double beta, int m = 0);
 int class_compress(sg_problem* P, const Factor& f, int l, const double* st, double** ctab);

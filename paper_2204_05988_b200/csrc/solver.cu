@@ -103,6 +103,8 @@ int pass1_vgroups(sg_problem* P, int l1, int l2, const double* X, double* const*
                 rc = launch_vfan_st(P, P->fv.d, S, n1, n2, Lv.so, Lx.bflag, vb, X, pitch);
             }
         }
+        if (rc == SG_ERR_UNSUPPORTED && P->use_vfan_k && !P->use_reg)
+            rc = launch_vfan_k(P, P->fv.d, S, n1, n2, Lv.so, Lx.bflag, vp, X, pitch);
         if (rc == SG_ERR_UNSUPPORTED && P->use_reg) rc = launch_vfan_reg(P, P->fv.d, S, n1, n2, Lv.so, Lx.bflag, vp, X);
         if (rc == SG_ERR_UNSUPPORTED) rc = launch_vfan_st(P, P->fv.d, S, n1, n2, Lv.so, Lx.bflag, vp, X, pitch);
         return rc;
