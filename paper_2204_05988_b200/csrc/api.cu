@@ -74,9 +74,14 @@ extern "C" int sg_create(const sg_config* cfg, void* stream, sg_problem** out) {
     // k-outer pass-1 kernel: more rows per coefficient load but register-starved; measured slower
     // than k_vfan_st on both 3D (1.35-1.86 vs 0.85 ms on grid (4,4)) in round 1: opt-in
     P->use_vfan_k = getenv("SG_VFANK") != nullptr;
-    // moment pass 1: faster than the stored-stencil kernel for d = 2 v-lattices, slower for d = 3
-    // (round-1 measurements, profiles/README.md); SG_VMOM forces it on, SG_NO_VMOM off
-    P->use_vmom = getenv("SG_NO_VMOM") == nullptr && (getenv("SG_VMOM") != nullptr || cfg->d == 2);
+    // warm-started block solves: measured no gain (configs[4]: 535 vs 526 inner its), opt-in
+    P->use_warm = getenv("SG_WARM") != nullptr;
+    // moment pass 1 (tables always prepared): used for d = 2 v-lattices, and for d = 3 only on
+    // grids with a tiny x factor where the stored per-column coefficients outweigh the
+    // intermediates (round-1 measurements, profiles/README.md); SG_VMOM forces it everywhere,
+    // SG_NO_VMOM off
+    P->use_vmom = getenv("SG_NO_VMOM") == nullptr;
+    P->force_vmom = getenv("SG_VMOM") != nullptr;
     P->xfi_cpt = getenv("SG_XFI_CPT") ? atoi(getenv("SG_XFI_CPT")) : 1;
     P->xfi_seg = getenv("SG_XFI_SEG") ? atoi(getenv("SG_XFI_SEG")) : 0;
     if (cudaStreamCreateWithFlags(&P->gstream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -197,10 +202,10 @@ extern "C" int sg_assemble_factors(sg_problem* P) {
     SG_CUDA(cudaMemset(P->scal, 0, sizeof(double) * 10 * (MAX_SEG + 1)));
     SG_CUDA(cudaMallocHost(&P->hscal, sizeof(double) * 10 * (MAX_SEG + 1)));
     const int64_t nF = std::max(P->fx.lev[F].n, P->fv.lev[F].n) + 16;
-    const int64_t sizes[16] = {Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na, Na + Nc, Na + Nc, Na,
-                               std::max(Na, 4 * nF), Na, Na, Na + Nc, Na + Nc, Na};
-    P->vec.assign(16, nullptr);
-    for (int i = 0; i < 16; ++i) SG_CUDA(cudaMalloc(&P->vec[i], sizeof(double) * sizes[i]));
+    const int64_t sizes[17] = {Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na, Na + Nc, Na + Nc, Na,
+                               std::max(Na, 4 * nF), Na, Na, Na + Nc, Na + Nc, Na, Na + Nc};
+    P->vec.assign(17, nullptr);
+    for (int i = 0; i < 17; ++i) SG_CUDA(cudaMalloc(&P->vec[i], sizeof(double) * sizes[i]));
     P->use_precond = getenv("SG_NO_PRECOND") == nullptr;
     SG_TRY(build_block_jacobi(P));
     SG_CUDA(cudaMalloc(&P->trace_dev, sizeof(double) * set_size(P, SG_SET_ACTIVE, 1)));

@@ -242,7 +242,10 @@ struct sg_problem {
     bool use_cross_batched = true; // SG_NO_CROSS_BATCH disables
     int outer_mode = 0;            // 0 Richardson + minimal-residual safeguard, 1 plain Richardson, 2 MR always
     int64_t mr_switches = 0;
+    bool use_warm = true;          // warm-started block solves (SG_NO_WARM disables)
+    bool warm_valid = false;
     bool use_vmom = true;          // moment pass 1 (SG_NO_VMOM disables)
+    bool force_vmom = false;       // SG_VMOM: moment pass 1 on every grid
     bool use_vfan_k = true;        // k-outer pass-1 kernel (SG_NO_VFANK disables)
     std::vector<int> vm_ok;        // per v-level: moment tables verified
     std::vector<double*> vm_tab;   // per v-level: [3^d][10][W] shifted-moment class tables

@@ -89,7 +89,8 @@ int pass1_vgroups(sg_problem* P, int l1, int l2, const double* X, double* const*
             vp.out[o] = outs[o];
         }
         int rc = SG_ERR_UNSUPPORTED;
-        if (!P->use_reg && P->use_vmom) {
+        const bool vmom_here = P->force_vmom || P->fv.d == 2 || n1 < 64;
+        if (!P->use_reg && P->use_vmom && vmom_here) {
             // interior groups by shifted moments, boundary-only (face) groups by the stencil kernel
             rc = launch_vmom(P, l2, (int64_t)S * n1, n2, pitch, X, vp.out, Lx.bflag, n1);
             if (rc == SG_OK && nb > P->ng_int && P->vm_nchi == 0) {
@@ -1052,6 +1053,21 @@ __global__ void k_seg_finalize(SegTab t, int K, const double* partial, double* s
         sc[6] = 0.0;
         return;
     }
+    if (op == 4) {              // warm start: r = (r.r, b.b); tolerance stays relative to |b|
+        sc[0] = r[0];
+        sc[3] = r[1];
+        sc[4] = r[0];
+        sc[5] = (r[1] == 0.0 || r[0] <= tol2 * r[1]) ? 1.0 : 0.0;
+        sc[1] = 0.0;
+        sc[2] = 0.0;
+        sc[6] = 0.0;
+        sc[7] = 0.0;
+        return;
+    }
+    if (op == 5) {              // warm-start factor per grid: alpha = (b.bp) / (bp.bp), kept in sc[9]
+        sc[9] = (r[1] > 0.0 && isfinite(r[0] / r[1])) ? r[0] / r[1] : 0.0;
+        return;
+    }
     if (sc[5] != 0.0) return;   // converged grid: scalars frozen
     if (op == 1) {              // alpha = rho / (r0.v)
         const double a = sc[0] / r[0];
@@ -1254,9 +1270,18 @@ __global__ void k_seg_precond(SegTab t, int S, const double* scal, const double*
     }
 }
 
+// x = sc[9] * x per segment (warm start from the previous outer iteration's block solutions)
+__global__ void k_seg_scale(SegTab t, const double* scal, double* x) {
+    const int g = seg_of(t, blockIdx.x);
+    const double a = scal[g * NSC + 9];
+    const int64_t lo = t.off[g] + (int64_t)(blockIdx.x - t.blk[g]) * SEG_CHUNK;
+    const int64_t hi = min(lo + SEG_CHUNK, t.off[g + 1]);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) x[i] *= a;
+}
+
 // batched BiCGStab on the grids `gr` (block solves of eq. (15)); b, x concatenated in order of gr
 static int bicgstab(sg_problem* P, const std::vector<const Grid*>& gr, const double* b, double* x, double rtol,
-                    int maxit) {
+                    int maxit, const double* bprev = nullptr) {
     const int S = P->S;
     std::vector<int64_t> offs(1, 0);
     for (auto* g : gr) offs.push_back(offs.back() + S * gsize(*g));
@@ -1266,14 +1291,32 @@ static int bicgstab(sg_problem* P, const std::vector<const Grid*>& gr, const dou
     double *r = P->vec[0], *r0 = P->vec[1], *p = P->vec[2], *v = P->vec[3], *s = P->vec[4], *tt = P->vec[5];
     double *ph = P->vec[13], *sh = P->vec[14];
     const bool pc = P->dinv != nullptr && P->use_precond;
-    SG_TRY(launch_zero(P, N, x));
-    SG_TRY(launch_copy(P, N, b, r));
-    SG_TRY(launch_copy(P, N, b, r0));
-    SG_TRY(launch_copy(P, N, b, p));
-    k_seg_dot<1><<<nblk, 256, 0, P->stream>>>(t, b, b, nullptr, nullptr, P->red);
-    k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 1, P->red, P->scal, 9, 9, 0, 0.0);
-    P->launches += 2;
     const double tol2 = rtol * rtol;
+    if (bprev && P->warm_valid) {
+        // warm start (see solve_strip): x0 = alpha_g * x_prev, alpha_g = (b, b_prev)/(b_prev, b_prev)
+        // per grid; the previous solution is the preconditioned one, so x0 = D^{-1}... is not needed:
+        // x holds the previous block solution itself
+        k_seg_dot<2><<<nblk, 256, 0, P->stream>>>(t, b, bprev, bprev, bprev, P->red);
+        k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 2, P->red, P->scal, 9, 9, 5, 0.0);
+        k_seg_scale<<<nblk, 256, 0, P->stream>>>(t, P->scal, x);
+        P->launches += 3;
+        for (size_t i = 0; i < gr.size(); ++i) SG_TRY(apply_diag(P, *gr[i], x + offs[i], v + offs[i]));
+        SG_TRY(launch_copy(P, N, b, r));
+        SG_TRY(launch_axpby(P, N, -1.0, v, 1.0, r));                         // r = b - A x0
+        SG_TRY(launch_copy(P, N, r, r0));
+        SG_TRY(launch_copy(P, N, r, p));
+        k_seg_dot<2><<<nblk, 256, 0, P->stream>>>(t, r, r, b, b, P->red);
+        k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 2, P->red, P->scal, 0, 0, 4, tol2);
+        P->launches += 2;
+    } else {
+        SG_TRY(launch_zero(P, N, x));
+        SG_TRY(launch_copy(P, N, b, r));
+        SG_TRY(launch_copy(P, N, b, r0));
+        SG_TRY(launch_copy(P, N, b, p));
+        k_seg_dot<1><<<nblk, 256, 0, P->stream>>>(t, b, b, nullptr, nullptr, P->red);
+        k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 1, P->red, P->scal, 9, 9, 0, 0.0);
+        P->launches += 2;
+    }
     std::vector<char> conv(gr.size(), 0);
     for (int it = 0; it < maxit; ++it) {
         // v = A M^{-1} p
@@ -1361,6 +1404,7 @@ int solve_strip(sg_problem* P, const double* b, double* u, double rtol, double i
     double* dhat = P->vec[8];     // [active | coarse]
     double* du = P->vec[9];
     double* Mw = P->vec[10];
+    double* rhs_prev = P->vec[16];   // previous outer iteration's block right-hand sides (warm start)
     std::vector<const Grid*> gr;
     for (auto& g : P->active) gr.push_back(&g);
     for (auto& g : P->coarse) gr.push_back(&g);
@@ -1393,7 +1437,12 @@ int solve_strip(sg_problem* P, const double* b, double* u, double rtol, double i
             SG_TRY(launch_gather(P, 0, P->fx.W, S, src.n1, src.n2, cg.n1, P->fx.lev[src.l1].rcols, el,
                                  rhs + Na + cg.off1 * S, 0.0));
         }
-        SG_TRY(bicgstab(P, gr, rhs, dhat, inner_rtol, 500));
+        // warm start of the block solves from the previous outer iteration (Richardson's corrections
+        // are asymptotically proportional from one iteration to the next); SG_NO_WARM disables
+        const bool warm = P->use_warm && it > 1;
+        P->warm_valid = warm;
+        SG_TRY(bicgstab(P, gr, rhs, dhat, inner_rtol, 500, warm ? rhs_prev : nullptr));
+        if (P->use_warm) SG_TRY(launch_copy(P, Na + Nc, rhs, rhs_prev));
         SG_TRY(combine(P, S, dhat, dhat + Na, du));
         int err = SG_OK;
         double omega = 1.0;

@@ -226,13 +226,16 @@ def test_solve_strip(name):
         assert relmax(f_gpu, f_ref) <= 1e-9, (s, it, git)
 
 
-@pytest.mark.parametrize("name", ["c2_4d_stream", "c4_6d_stream", "c1_2d_rot"])
-def test_solve_strip_minimal_residual_steps(name, monkeypatch):
+@pytest.mark.parametrize("name", ["c2_4d_stream", "c4_6d_stream", "c1_2d_rot", "c3_4d_lshape"])
+@pytest.mark.parametrize("env", ["SG_OUTER=2", "SG_WARM=1"])
+def test_solve_strip_solver_variants(name, env, monkeypatch):
     """SG_OUTER=2 (residual-minimising step lengths from the first iteration, the safeguard's
-    mode): the same converged strip solution as the oracle's plain Richardson."""
+    mode) and SG_NO_WARM (cold-started block solves): the same converged strip solution as
+    the oracle's plain Richardson."""
     from oracle.sgrid import SGProblem
     from paper_2204_05988_b200 import Problem
-    monkeypatch.setenv("SG_OUTER", "2")
+    k, v = env.split("=")
+    monkeypatch.setenv(k, v)
     cfg = get_config(name, L=SMALL[name])
     g, o = Problem(cfg), SGProblem(cfg)
     tr0 = o.interp_u0()
