@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(256, 2)
             double xv[VR];
 #pragma unroll
             for (int r = 0; r < VR; ++r)
-                xv[r] = (nb_ok[k] && rb + r < nrows) ? __ldg(xb + (long long)r * n2 + cf.off[k]) : 0.0;
+                xv[r] = (nb_ok[k] && rb + r < nrows) ? __ldg(xb + (r * n2 + cf.off[k])) : 0.0;
 #pragma unroll
             for (int n = 0; n < VM_NP; ++n) {
                 if (!vm::mono_in(D, n)) continue;
@@ -159,8 +159,11 @@ __global__ void __launch_bounds__(256, 2)
             vm_combine<D>(zr, y, o, idx);
             const bool xb_row = cf.nchi && xflag[row % n1x];
             if (xb_row) {
-                // chi groups: half stencils need the row's X values again (plane rows only)
-                for (int c = 0; c < cf.nchi; ++c) {
+                // chi groups (unrolled for d = 2: compile-time parameter offsets; rolled for d = 3,
+                // where unrolling spills); half stencils need the row's X values again (plane rows only)
+#pragma unroll(D == 2 ? VM_NC : 1)
+                for (int c = 0; c < VM_NC; ++c) {
+                    if (c >= cf.nchi) break;
                     const int i = cf.chax[c];
                     const double yi = i == 0 ? y[0] : (i == 1 ? y[1] : y[2]);
                     const double zi = i == 0 ? zr[1] : (i == 1 ? zr[2] : zr[3]);
