@@ -19,6 +19,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -113,7 +114,7 @@ constexpr int XFT_MAXG = 12;
 // coefficient loads are warp-uniform and go through the constant cache, not L1
 constexpr int XFT_CTAB = 27 * 10 * 15;   // interior groups only (bonly groups read the global table)
 __constant__ double c_xft[XFT_CTAB];
-constexpr int XFT_NST = 4;   // pipeline stages
+constexpr int XFT_MAXST = 12;   // pipeline stages (runtime, sized to the shared-memory budget)
 struct XftCoef {
     double c[XFT_MAXG][15];
 };
@@ -121,6 +122,7 @@ struct XftTile {
     int wl1, wl2, wc, nw;      // warp blocks per tile (axis 1, axis 2), column groups, consumer warps
     int e1, e2, bc;            // stage box: halo lines (axis 1, axis 2), columns
     int ntl1, ntl2, nct, nseg, seglen;
+    int nst;                   // pipeline depth
 };
 
 template <int D, int NGI, bool CTAB>
@@ -132,8 +134,9 @@ __global__ void __launch_bounds__(32 * 17, 1)
     extern __shared__ __align__(128) unsigned char smraw[];
     const int stage_elems = tl.e1 * tl.e2 * tl.bc;
     double* stages = reinterpret_cast<double*>(smraw);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smraw + (size_t)XFT_NST * stage_elems * 8);
-    uint64_t* empty = full + XFT_NST;
+    const int nst = tl.nst;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smraw + (size_t)nst * stage_elems * 8);
+    uint64_t* empty = full + nst;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // CTA -> (line tile, segment, column tile)
@@ -152,7 +155,7 @@ __global__ void __launch_bounds__(32 * 17, 1)
                                (D == 2 || (L2 >= 1 && L2 + tl.wl2 * G::B2 - 1 <= m - 2));
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < XFT_NST; ++i) {
+        for (int i = 0; i < nst; ++i) {
             xft::mbar_init(&full[i], 1);
             xft::mbar_init(&empty[i], tl.nw);
         }
@@ -164,13 +167,18 @@ __global__ void __launch_bounds__(32 * 17, 1)
         // ---------------- producer: one elected lane issues the TMA loads
         if (lane == 0) {
             const uint32_t bytes = (uint32_t)stage_elems * 8u;
-            int q = 0;
+            int q = 0, pb = 0;
+            uint32_t pph = 0;
             for (int t = ts; t <= te; ++t) {
                 const bool cint_t = cta_lines_int && t >= 2 && t <= m - 3;
                 const int ng = cint_t ? NGI : nga;
                 for (int g = 0; g < ng; ++g, ++q) {
-                    const int b = q % XFT_NST;
-                    if (q >= XFT_NST) xft::mbar_wait(&empty[b], ((q / XFT_NST) - 1) & 1);
+                    const int b = pb;
+                    if (q >= nst) xft::mbar_wait(&empty[b], pph ^ 1u);
+                    if (++pb == nst) {
+                        pb = 0;
+                        pph ^= 1u;
+                    }
                     xft::mbar_expect_tx(&full[b], bytes);
                     if (D == 3)
                         xft::tma_load<3>(stages + (size_t)b * stage_elems, &tmap, &full[b], ct * tl.bc, t, L1 - 1,
@@ -215,7 +223,8 @@ __global__ void __launch_bounds__(32 * 17, 1)
 #pragma unroll
     for (int u = 0; u < NT; ++u) acc[u][0] = acc[u][1] = acc[u][2] = 0.0;
 
-    int q = 0;
+    int q = 0, cbuf = 0;
+    uint32_t cph = 0;
     for (int t = ts; t <= te; ++t) {
         const bool cint_t = cta_lines_int && t >= 2 && t <= m - 3;
         const bool wint = lines_int && t >= 2 && t <= m - 3;
@@ -231,8 +240,12 @@ __global__ void __launch_bounds__(32 * 17, 1)
             }
 #pragma unroll
         for (int g = 0; g < NGI; ++g, ++q) {
-            const int b = q % XFT_NST;
-            xft::mbar_wait(&full[b], (q / XFT_NST) & 1);
+            const int b = cbuf;
+            xft::mbar_wait(&full[b], cph);
+            if (++cbuf == nst) {
+                cbuf = 0;
+                cph ^= 1u;
+            }
             const double* st = stages + (size_t)b * stage_elems;
             double src[NS];
 #pragma unroll
@@ -270,8 +283,12 @@ __global__ void __launch_bounds__(32 * 17, 1)
         }
         if (!cint_t) {
             for (int g = NGI; g < nga; ++g, ++q) {
-                const int b = q % XFT_NST;
-                xft::mbar_wait(&full[b], (q / XFT_NST) & 1);
+                const int b = cbuf;
+                xft::mbar_wait(&full[b], cph);
+                if (++cbuf == nst) {
+                    cbuf = 0;
+                    cph ^= 1u;
+                }
                 if (!wint) {
                     const double* st = stages + (size_t)b * stage_elems;
                     const double* tg = tab + g * W;
@@ -408,7 +425,11 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
     }
     XftCoef ci;
     std::memcpy(ci.c, P->xfi_cint[l1].data(), sizeof(ci.c));
-    const size_t smem = (size_t)XFT_NST * tl.e1 * tl.e2 * tl.bc * 8 + 2 * XFT_NST * sizeof(uint64_t);
+    const size_t stage_b = (size_t)tl.e1 * tl.e2 * tl.bc * 8;
+    // 4 stages measured best (deeper rings shrink L1 and were slower: (2,6) 3.3 -> 5.1 ms at 8 stages)
+    tl.nst = P->xft_smem_kb > 0 ? (int)std::min<size_t>(XFT_MAXST, std::max<size_t>(2, (size_t)(P->xft_smem_kb * 1024) / stage_b))
+                                : 4;
+    const size_t smem = (size_t)tl.nst * stage_b + 2 * tl.nst * sizeof(uint64_t);
     {
         int ncls = 1;
         for (int q = 0; q < d; ++q) ncls *= 3;
