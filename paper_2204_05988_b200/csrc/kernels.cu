@@ -1071,7 +1071,105 @@ __global__ void __launch_bounds__(256) k_jobs(JobList jl) {
     }
 }
 
+// Warp-unit variant: a warp owns one unit of a job —
+//   dir 0 (transfer along the x rows): one output row r and a chunk of JB_CH columns; the
+//         row's W (col, val) pairs are loaded once and every lane streams columns;
+//   dir 1 (transfer along the v columns): 32 output columns (lane = column) and JB_RC rows;
+//         each lane loads its column's W pairs once and streams the rows.
+// No per-element index division; coefficient/pattern loads amortised over the unit.
+constexpr int JB_CH = 1024, JB_RC = 16;
+__device__ __forceinline__ int64_t job_units(const Job& J) {
+    if (J.dir == 0) return (int64_t)J.S * J.nrows_out * ((J.n2_in + JB_CH - 1) / JB_CH);
+    return ((J.nrows_out + 31) / 32) * (((int64_t)J.S * J.n1_in + JB_RC - 1) / JB_RC);
+}
+__global__ void __launch_bounds__(256) k_jobs2(JobList jl) {
+    int j = 0;
+    while (j + 1 < jl.nj && jl.j[j + 1].blk0 <= (int)blockIdx.x) ++j;
+    const Job& J = jl.j[j];
+    const int lane = threadIdx.x & 31;
+    const int64_t u = (int64_t)(blockIdx.x - J.blk0) * 8 + (threadIdx.x >> 5);
+    if (u >= job_units(J)) return;
+    const int W = J.W;
+    if (J.dir == 0) {
+        const int64_t n2 = J.n2_in, nch = (n2 + JB_CH - 1) / JB_CH;
+        const int64_t rowidx = u / nch, ch = u - rowidx * nch;
+        const int64_t s = rowidx / J.nrows_out, r = rowidx - s * J.nrows_out;
+        int32_t col[15];
+        double val[15];
+#pragma unroll
+        for (int k = 0; k < 15; ++k) {
+            col[k] = k < W ? __ldg(J.cols + k * J.nrows_out + r) : -1;
+            val[k] = k < W && col[k] >= 0 ? __ldg(J.vals + k * J.nrows_out + r) : 0.0;
+        }
+        const double* in = J.in + (size_t)s * J.n1_in * n2;
+        const int64_t obase = (s * J.nrows_out + r) * (J.opitch > 0 ? J.opitch : n2);
+        const int64_t abase = (s * J.nrows_out + r) * n2;
+        const int64_t c1 = min(n2, (ch + 1) * JB_CH);
+#pragma unroll 4
+        for (int64_t c = ch * JB_CH + lane; c < c1; c += 32) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < 15; ++k)
+                if (k < W && col[k] >= 0) acc = fma(val[k], __ldg(in + (size_t)col[k] * n2 + c), acc);
+            J.out[obase + c] = (J.add ? J.add[abase + c] : 0.0) + J.scale * acc;
+        }
+    } else {
+        const int64_t nct = (J.nrows_out + 31) / 32;
+        const int64_t rc = u / nct, ct = u - rc * nct;
+        const int64_t c = ct * 32 + lane;
+        if (c >= J.nrows_out) return;
+        int32_t col[15];
+        double val[15];
+#pragma unroll
+        for (int k = 0; k < 15; ++k) {
+            col[k] = k < W ? __ldg(J.cols + k * J.nrows_out + c) : -1;
+            val[k] = k < W && col[k] >= 0 ? __ldg(J.vals + k * J.nrows_out + c) : 0.0;
+        }
+        const int64_t nrows = (int64_t)J.S * J.n1_in;
+        const int64_t r1 = min(nrows, (rc + 1) * JB_RC);
+        const int64_t op = J.opitch > 0 ? J.opitch : J.nrows_out;
+#pragma unroll 4
+        for (int64_t rr = rc * JB_RC; rr < r1; ++rr) {
+            const double* in = J.in + rr * J.n2_in;
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < 15; ++k)
+                if (k < W && col[k] >= 0) acc = fma(val[k], __ldg(in + col[k]), acc);
+            J.out[rr * op + c] = (J.add ? J.add[rr * J.nrows_out + c] : 0.0) + J.scale * acc;
+        }
+    }
+}
+
 int launch_jobs(sg_problem* P, std::vector<Job>& jobs) {
+    if (P->use_jobs2) {
+        size_t i = 0;
+        while (i < jobs.size()) {
+            JobList jl;
+            jl.nj = 0;
+            int blk = 0;
+            while (i < jobs.size() && jl.nj < MAX_JOBS) {
+                Job J = jobs[i++];
+                if (J.W > 15) {
+                    set_error("transfer job wider than 15");
+                    return SG_ERR_UNSUPPORTED;
+                }
+                int64_t units = J.dir == 0 ? (int64_t)J.S * J.nrows_out * ((J.n2_in + JB_CH - 1) / JB_CH)
+                                           : ((J.nrows_out + 31) / 32) * (((int64_t)J.S * J.n1_in + JB_RC - 1) / JB_RC);
+                if (units == 0) continue;
+                const int64_t nb = (units + 7) / 8;
+                if (nb + blk >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
+                J.blk0 = blk;
+                blk += (int)nb;
+                jl.j[jl.nj++] = J;
+            }
+            if (jl.nj == 0) continue;
+            jl.total_blocks = blk;
+            k_jobs2<<<blk, 256, 0, P->stream>>>(jl);
+            P->launches++;
+            SG_CUDA(cudaGetLastError());
+        }
+        return SG_OK;
+    }
     size_t i = 0;
     while (i < jobs.size()) {
         JobList jl;

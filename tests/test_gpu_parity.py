@@ -120,7 +120,7 @@ def test_apply_full_cross_grid(name):
         assert relmax(Y[l], ref[l]) <= 1e-12, l
 
 
-@pytest.mark.parametrize("env", ["SG_NO_CROSS_BATCH", "SG_NO_TMA", "SG_VMOM"])
+@pytest.mark.parametrize("env", ["SG_NO_CROSS_BATCH", "SG_NO_TMA", "SG_VMOM", "SG_JOBS2"])
 @pytest.mark.parametrize("name", ["c2_4d_stream", "c4_6d_stream"])
 def test_apply_full_cross_grid_paths(name, env, monkeypatch):
     """Cross-grid apply on the per-group path and with the batched lower part's kernel variants."""
