@@ -1151,6 +1151,37 @@ __global__ void k_bicg_xr(SegTab tb, const double* scal, double* x, double* r, c
     }
 }
 
+// fused S = 1 variants with the point-Jacobi preconditioner: s = r - alpha v, sh = D^{-1} s
+__global__ void k_bicg_s_pc(SegTab t, const double* scal, const double* r, const double* v, double* s,
+                            const double* Dinv, double* sh) {
+    const int g = seg_of(t, blockIdx.x);
+    const double* sc = scal + g * NSC;
+    if (sc[5] != 0.0) return;
+    const double al = sc[1];
+    const int64_t lo = t.off[g] + (int64_t)(blockIdx.x - t.blk[g]) * SEG_CHUNK;
+    const int64_t hi = min(lo + SEG_CHUNK, t.off[g + 1]);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const double si = r[i] - al * v[i];
+        s[i] = si;
+        sh[i] = Dinv[i] * si;
+    }
+}
+// p = r + beta (p - omega v), ph = D^{-1} p (the next iteration's preconditioned direction)
+__global__ void k_bicg_p_pc(SegTab t, const double* scal, double* p, const double* r, const double* v,
+                            const double* Dinv, double* ph) {
+    const int g = seg_of(t, blockIdx.x);
+    const double* sc = scal + g * NSC;
+    if (sc[5] != 0.0) return;
+    const double be = sc[6], om = sc[2];
+    const int64_t lo = t.off[g] + (int64_t)(blockIdx.x - t.blk[g]) * SEG_CHUNK;
+    const int64_t hi = min(lo + SEG_CHUNK, t.off[g + 1]);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const double pi = r[i] + be * (p[i] - om * v[i]);
+        p[i] = pi;
+        ph[i] = Dinv[i] * pi;
+    }
+}
+
 // p = r + beta (p - omega v)
 __global__ void k_bicg_p(SegTab t, const double* scal, double* p, const double* r, const double* v) {
     const int g = seg_of(t, blockIdx.x);
@@ -1291,6 +1322,7 @@ static int bicgstab(sg_problem* P, const std::vector<const Grid*>& gr, const dou
     double *r = P->vec[0], *r0 = P->vec[1], *p = P->vec[2], *v = P->vec[3], *s = P->vec[4], *tt = P->vec[5];
     double *ph = P->vec[13], *sh = P->vec[14];
     const bool pc = P->dinv != nullptr && P->use_precond;
+    const bool fuse = pc && S == 1;   // preconditioner fused into the s / p updates
     const double tol2 = rtol * rtol;
     if (bprev && P->warm_valid) {
         // warm start (see solve_strip): x0 = alpha_g * x_prev, alpha_g = (b, b_prev)/(b_prev, b_prev)
@@ -1320,22 +1352,29 @@ static int bicgstab(sg_problem* P, const std::vector<const Grid*>& gr, const dou
     std::vector<char> conv(gr.size(), 0);
     for (int it = 0; it < maxit; ++it) {
         // v = A M^{-1} p
-        const double* pa = p;
+            const double* pa = p;
         if (pc) {
-            k_seg_precond<<<nblk, 256, 0, P->stream>>>(t, S, P->scal, P->dinv, p, ph);
-            P->launches++;
+            if (!fuse || it == 0) {   // fused path: ph was produced by k_bicg_p_pc of the last iteration
+                k_seg_precond<<<nblk, 256, 0, P->stream>>>(t, S, P->scal, P->dinv, p, ph);
+                P->launches++;
+            }
             pa = ph;
         }
         for (size_t i = 0; i < gr.size(); ++i)
             if (!conv[i]) SG_TRY(apply_diag(P, *gr[i], pa + offs[i], v + offs[i]));
         k_seg_dot<1><<<nblk, 256, 0, P->stream>>>(t, r0, v, nullptr, nullptr, P->red, nullptr, nullptr, P->scal);
         k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 1, P->red, P->scal, 6, 6, 1, tol2);
-        k_bicg_s<<<nblk, 256, 0, P->stream>>>(t, P->scal, r, v, s);
         const double* sa = s;
-        if (pc) {
-            k_seg_precond<<<nblk, 256, 0, P->stream>>>(t, S, P->scal, P->dinv, s, sh);
-            P->launches++;
+        if (fuse) {
+            k_bicg_s_pc<<<nblk, 256, 0, P->stream>>>(t, P->scal, r, v, s, P->dinv, sh);
             sa = sh;
+        } else {
+            k_bicg_s<<<nblk, 256, 0, P->stream>>>(t, P->scal, r, v, s);
+            if (pc) {
+                k_seg_precond<<<nblk, 256, 0, P->stream>>>(t, S, P->scal, P->dinv, s, sh);
+                P->launches++;
+                sa = sh;
+            }
         }
         for (size_t i = 0; i < gr.size(); ++i)
             if (!conv[i]) SG_TRY(apply_diag(P, *gr[i], sa + offs[i], tt + offs[i]));
@@ -1343,7 +1382,10 @@ static int bicgstab(sg_problem* P, const std::vector<const Grid*>& gr, const dou
         k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 3, P->red, P->scal, 7, 8, 2, tol2);
         k_bicg_xr<<<nblk, 256, 0, P->stream>>>(t, P->scal, x, r, pa, sa, s, tt, r0, P->red);
         k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 2, P->red, P->scal, 0, 4, 3, tol2);
-        k_bicg_p<<<nblk, 256, 0, P->stream>>>(t, P->scal, p, r, v);
+        if (fuse)
+            k_bicg_p_pc<<<nblk, 256, 0, P->stream>>>(t, P->scal, p, r, v, P->dinv, ph);
+        else
+            k_bicg_p<<<nblk, 256, 0, P->stream>>>(t, P->scal, p, r, v);
         P->launches += 8;
         SG_CUDA(cudaGetLastError());
         P->inner_iters++;
