@@ -346,20 +346,21 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // tile choice: minimise TMA source-line loads per valid target line
-static XftTile choose_tile(int d, int m, int64_t n2, int ngi_total_work_hint) {
+static XftTile choose_tile(int d, int m, int64_t n2, int force_wc, int box_kb) {
     XftTile best{};
     double best_cost = 1e30;
     const int B1 = d == 3 ? 2 : 4;
     const int lines1 = m, lines2 = d == 3 ? m : 1;
     for (int wc = 1; wc <= 4; wc *= 2) {
         if (wc > 1 && n2 < 32LL * wc) continue;
+        if (force_wc > 0 && wc != force_wc) continue;
         for (int w1 = 1; w1 <= 16; ++w1)
             for (int w2 = 1; w2 <= (d == 3 ? 16 : 1); ++w2) {
                 const int nw = w1 * w2 * wc;
                 if (nw < 4 || nw > 16) continue;
                 const int e1 = w1 * B1 + 2, e2 = d == 3 ? w2 * 2 + 2 : 1;
                 const int bc = 32 * wc;
-                if ((double)e1 * e2 * bc * 8 > 24 * 1024) continue;
+                if ((double)e1 * e2 * bc * 8 > box_kb * 1024.0) continue;
                 const int nt1 = (lines1 + w1 * B1 - 1) / (w1 * B1);
                 const int nt2 = d == 3 ? (lines2 + w2 * 2 - 1) / (w2 * 2) : 1;
                 const int64_t nct = (n2 + bc - 1) / bc;
@@ -372,7 +373,6 @@ static XftTile choose_tile(int d, int m, int64_t n2, int ngi_total_work_hint) {
                 }
             }
     }
-    (void)ngi_total_work_hint;
     return best;
 }
 
@@ -385,7 +385,11 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
         return SG_ERR_UNSUPPORTED;
     auto enc = get_encode();
     if (!enc) return SG_ERR_UNSUPPORTED;
-    XftTile tl = choose_tile(d, m, n2, 0);
+    // wide boxes (4 column groups = 1 KB rows) measured fastest on the m >= 9 lattices
+    // (grid (5,3): 1.67 -> 1.25 ms) and slowest on m = 5 (3.3 -> 4.7 ms)
+    const int wc_auto = (m >= 9 && n2 >= 128) ? 4 : 0;
+    XftTile tl = choose_tile(d, m, n2, P->xft_wc > 0 ? P->xft_wc : wc_auto, P->xft_box_kb);
+    if (tl.nw == 0) tl = choose_tile(d, m, n2, 0, 24);
     // split the sweep until there are >= 2 CTAs per SM
     const int64_t base = (int64_t)tl.ntl1 * tl.ntl2 * tl.nct;
     int seglen = P->xfi_seg > 0 ? P->xfi_seg : m;
