@@ -346,6 +346,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // tile choice: minimise TMA source-line loads per valid target line
+static int g_xft_minw = 4;
 static XftTile choose_tile(int d, int m, int64_t n2, int force_wc, int box_kb) {
     XftTile best{};
     double best_cost = 1e30;
@@ -357,7 +358,7 @@ static XftTile choose_tile(int d, int m, int64_t n2, int force_wc, int box_kb) {
         for (int w1 = 1; w1 <= 16; ++w1)
             for (int w2 = 1; w2 <= (d == 3 ? 16 : 1); ++w2) {
                 const int nw = w1 * w2 * wc;
-                if (nw < 4 || nw > 16) continue;
+                if (nw < g_xft_minw || nw > 16) continue;
                 const int e1 = w1 * B1 + 2, e2 = d == 3 ? w2 * 2 + 2 : 1;
                 const int bc = 32 * wc;
                 if ((double)e1 * e2 * bc * 8 > box_kb * 1024.0) continue;
@@ -388,7 +389,11 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
     // wide boxes (4 column groups = 1 KB rows) measured fastest on the m >= 9 lattices
     // (grid (5,3): 1.67 -> 1.25 ms) and slowest on m = 5 (3.3 -> 4.7 ms)
     const int wc_auto = (m >= 9 && n2 >= 128) ? 4 : 0;
-    XftTile tl = choose_tile(d, m, n2, P->xft_wc > 0 ? P->xft_wc : wc_auto, P->xft_box_kb);
+    g_xft_minw = getenv("SG_XFT_MINW") ? atoi(getenv("SG_XFT_MINW")) : 4;
+    // ... and small CTAs (one 2x2 line block x 4 column groups, 16 KB stages) beat larger tiles
+    // on those lattices: more independent TMA producers per SM (grid (3,5): 2.02 -> 1.82 ms)
+    const int box_kb = getenv("SG_XFT_BOX_KB") ? P->xft_box_kb : (wc_auto ? 16 : 24);
+    XftTile tl = choose_tile(d, m, n2, P->xft_wc > 0 ? P->xft_wc : wc_auto, box_kb);
     if (tl.nw == 0) tl = choose_tile(d, m, n2, 0, 24);
     // split the sweep until there are >= 2 CTAs per SM
     const int64_t base = (int64_t)tl.ntl1 * tl.ntl2 * tl.nct;
