@@ -18,18 +18,19 @@
 
 namespace sg {
 
+// (index arithmetic in 32 bits: every caller has S * n1 * n2 < 2^31 and S <= 2, checked on the host)
 template <int DIR, int W, int NO>
 __global__ void __launch_bounds__(256) k_fanout(int S, int64_t n1, int64_t n2_in, int64_t n1_out, int64_t n2_out,
                                                 const int32_t* __restrict__ cols, const double* __restrict__ in,
                                                 FanoutList fl, int o0) {
-    const int64_t per_s = n1_out * n2_out;
-    const int64_t total = per_s * S;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int s = (int)(t / per_s);
-        const int64_t rc = t - s * per_s;
-        const int64_t r = rc / n2_out;
-        const int64_t c = rc - r * n2_out;
+    const unsigned per_s = (unsigned)(n1_out * n2_out);
+    const unsigned total = per_s * (unsigned)S;
+    const unsigned n2o = (unsigned)n2_out;
+    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int s = t >= per_s ? 1 : 0;
+        const unsigned rc = t - s * per_s;
+        const int64_t r = rc / n2o;
+        const int64_t c = rc - (unsigned)r * n2o;
         double x[W];
         int64_t row;
         int64_t nrows;
@@ -65,14 +66,14 @@ template <int DIR, int W>
 __global__ void __launch_bounds__(256) k_gather(int S_out, int64_t n1_in, int64_t n2_in, int64_t n1_out,
                                                 int64_t n2_out, const int32_t* __restrict__ cols, EntryList el,
                                                 double* __restrict__ out, double beta) {
-    const int64_t per_s = n1_out * n2_out;
-    const int64_t total = per_s * S_out;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int s = (int)(t / per_s);
-        const int64_t rc = t - s * per_s;
-        const int64_t r = rc / n2_out;
-        const int64_t c = rc - r * n2_out;
+    const unsigned per_s = (unsigned)(n1_out * n2_out);
+    const unsigned total = per_s * (unsigned)S_out;
+    const unsigned n2o = (unsigned)n2_out;
+    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int s = t >= per_s ? 1 : 0;
+        const unsigned rc = t - s * per_s;
+        const int64_t r = rc / n2o;
+        const int64_t c = rc - (unsigned)r * n2o;
         const int64_t nrows = DIR == 1 ? n2_out : n1_out;
         const int64_t row = DIR == 1 ? c : r;
         int32_t cl[W];
@@ -134,6 +135,10 @@ int launch_fanout(sg_problem* P, int dir, int W, int S, int64_t n1_in, int64_t n
     const int64_t n1_out = dir == 0 ? nrows_out : n1_in;
     const int64_t n2_out = dir == 1 ? nrows_out : n2_in;
     if (n1_out * n2_out == 0 || fl.no == 0) return SG_OK;
+    if ((int64_t)S * n1_out * n2_out >= (1LL << 31) || S > 2) {
+        set_error("fanout too large for 32-bit indexing");
+        return SG_ERR_UNSUPPORTED;
+    }
 #define FO(D, WW) fanout_dispatch<D, WW>(P, S, n1_in, n2_in, n1_out, n2_out, cols, in, fl)
     if (dir == 1) {
         if (W == 3) FO(1, 3); else if (W == 7) FO(1, 7); else if (W == 15) FO(1, 15); else if (W == 2) FO(1, 2);
@@ -153,6 +158,10 @@ int launch_gather(sg_problem* P, int dir, int W, int S_out, int64_t n1_in, int64
     const int64_t n2_out = dir == 1 ? nrows_out : n2_in;
     const int64_t total = (int64_t)S_out * n1_out * n2_out;
     if (total == 0) return SG_OK;
+    if (total >= (1LL << 31) || S_out > 2) {
+        set_error("gather too large for 32-bit indexing");
+        return SG_ERR_UNSUPPORTED;
+    }
     const int g = grid_for(total);
 #define GA(D, WW) k_gather<D, WW><<<g, 256, 0, P->stream>>>(S_out, n1_in, n2_in, n1_out, n2_out, cols, el, out, beta)
     if (dir == 1) {
