@@ -115,7 +115,7 @@ struct Group {                 // terms sharing one spec on the "inner" factor
     std::vector<std::vector<CombEntry>> comb;
 };
 
-constexpr int MAXG = 24;
+constexpr int MAXG = 40;   // v-groups handled by the stencil pass-1 kernels (configs[3] has > 24)
 struct VfanParams {
     int ng, ng_int;
     const double* vst[MAXG];
