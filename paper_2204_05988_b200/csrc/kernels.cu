@@ -64,8 +64,9 @@ __global__ void __launch_bounds__(256) k_fanout(int S, int64_t n1, int64_t n2_in
 
 template <int DIR, int W>
 __global__ void __launch_bounds__(256) k_gather(int S_out, int64_t n1_in, int64_t n2_in, int64_t n1_out,
-                                                int64_t n2_out, const int32_t* __restrict__ cols, EntryList el,
-                                                double* __restrict__ out, double beta) {
+                                                int64_t n2_out, const int32_t* __restrict__ cols,
+                                                const __grid_constant__ EntryList el, double* __restrict__ out,
+                                                double beta) {
     const unsigned per_s = (unsigned)(n1_out * n2_out);
     const unsigned total = per_s * (unsigned)S_out;
     const unsigned n2o = (unsigned)n2_out;
@@ -80,8 +81,7 @@ __global__ void __launch_bounds__(256) k_gather(int S_out, int64_t n1_in, int64_
 #pragma unroll
         for (int k = 0; k < W; ++k) cl[k] = __ldg(cols + k * nrows + row);
         double acc = 0.0;
-        for (int e = 0; e < el.ne; ++e) {
-            if (el.e[e].s_out != s) continue;
+        for (int e = el.sbeg[s]; e < el.sbeg[s + 1]; ++e) {
             const double* v = el.e[e].vals;
             const double* base;
             if (DIR == 1)
@@ -153,7 +153,16 @@ int launch_fanout(sg_problem* P, int dir, int W, int S, int64_t n1_in, int64_t n
 }
 
 int launch_gather(sg_problem* P, int dir, int W, int S_out, int64_t n1_in, int64_t n2_in, int64_t nrows_out,
-                  const int32_t* cols, const EntryList& el, double* out, double beta) {
+                  const int32_t* cols, const EntryList& el_in, double* out, double beta) {
+    // entries grouped by output time component (each thread only walks its own s_out)
+    EntryList el;
+    el.ne = 0;
+    for (int s = 0; s < S_out && s < 2; ++s) {
+        el.sbeg[s] = el.ne;
+        for (int e = 0; e < el_in.ne; ++e)
+            if (el_in.e[e].s_out == s) el.e[el.ne++] = el_in.e[e];
+    }
+    for (int s = std::min(S_out, 2); s <= 2; ++s) el.sbeg[s] = el.ne;
     const int64_t n1_out = dir == 0 ? nrows_out : n1_in;
     const int64_t n2_out = dir == 1 ? nrows_out : n2_in;
     const int64_t total = (int64_t)S_out * n1_out * n2_out;

@@ -14,7 +14,7 @@ namespace sg {
 constexpr int MAXD = 3;
 constexpr int NPOLY = 10;   // [1, y0, y1, y2, y0y0, y0y1, y0y2, y1y1, y1y2, y2y2]
 constexpr int MAXS = 2;     // q <= 1
-constexpr int MAX_ENTRIES = 64;
+constexpr int MAX_ENTRIES = 128;   // gather entries per launch (kernel parameter space allows > 4 KB on sm_100)
 constexpr int MAX_FANOUT = 12;
 constexpr int MAX_SEG = 64;
 
@@ -92,6 +92,7 @@ struct Entry {
 };
 struct EntryList {
     int ne;
+    int sbeg[3];   // entries sorted by s_out: [sbeg[s], sbeg[s+1]) (set by launch_gather)
     Entry e[MAX_ENTRIES];
 };
 struct FanoutList {
