@@ -53,11 +53,6 @@ static Poly pmul(const Poly& p, const Poly& q) {   // deg(p), deg(q) <= 1
         for (int j = 0; j < 3; ++j) r.c[qidx(i, j)] += p.c[1 + i] * q.c[1 + j];
     return r;
 }
-static bool pzero(const Poly& p) {
-    for (double v : p.c)
-        if (v != 0.0) return false;
-    return true;
-}
 
 struct SpaceTerm {
     Spec x, v;

@@ -359,7 +359,7 @@ namespace sg {
 // c_xw[g][r][k] with (r, k) compile-time and g warp-uniform (uniform constant
 // loads, no L1 traffic), and absent neighbours are dropped at compile time.
 // =====================================================================
-constexpr int XW_MAXG = 16, XW_MAXN = 27, XW_MAXW = 15;
+constexpr int XW_MAXG = 16, XW_MAXN = 27;
 constexpr int XW_MAXP = 223;   // valid (row, offset) pairs of the 3^3 lattice (3^2: 41, 5^2: 137)
 
 namespace xw {
@@ -501,7 +501,7 @@ int prepare_xwhole(sg_problem* P) {
 int launch_xwhole(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pitch, const double* Z, int64_t gstride,
                   double* Y) {
     if (l1 >= (int)P->xfi_tab.size() || !P->xfi_tab[l1]) return SG_ERR_UNSUPPORTED;
-    const int d = P->fx.d, m = P->fx.lev[l1].m, W = P->fx.W;
+    const int d = P->fx.d, m = P->fx.lev[l1].m;
     const int nga = (int)P->vorder.size();
     const bool ok = (d == 3 && m == 3) || (d == 2 && (m == 3 || m == 5));
     if (!ok || nga > XW_MAXG || n1 * n2 >= (1LL << 31) || n1 > XW_MAXN) return SG_ERR_UNSUPPORTED;
