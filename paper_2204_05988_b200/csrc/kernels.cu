@@ -101,6 +101,49 @@ __global__ void __launch_bounds__(256) k_gather(int S_out, int64_t n1_in, int64_
     }
 }
 
+// x-side gather for S_out = 2 (dG(1)): one thread produces both time components of (r, c), and
+// entries sharing an input (same group and s_in, consecutive after the host sort) reuse the W
+// loaded values, so every intermediate value is read once per output node instead of S_out times.
+template <int W>
+__global__ void __launch_bounds__(256) k_gather_s2(int64_t n1_in, int64_t n2_in, int64_t n1_out,
+                                                   const int32_t* __restrict__ cols,
+                                                   const __grid_constant__ EntryList el, double* __restrict__ out,
+                                                   double beta) {
+    const unsigned n2o = (unsigned)n2_in;
+    const unsigned per_s = (unsigned)(n1_out * n2_in);
+    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < per_s; t += gridDim.x * blockDim.x) {
+        const unsigned r = t / n2o, c = t - r * n2o;
+        int32_t cl[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) cl[k] = __ldg(cols + (size_t)k * n1_out + r);
+        double acc0 = 0.0, acc1 = 0.0;
+        double xv[W];
+        const double* prev = nullptr;
+        int prev_s = -1;
+        for (int e = 0; e < el.ne; ++e) {
+            const Entry& E = el.e[e];
+            if (E.in != prev || E.s_in != prev_s) {
+                prev = E.in;
+                prev_s = E.s_in;
+                const double* base = E.in + (size_t)E.s_in * n1_in * n2_in + c;
+#pragma unroll
+                for (int k = 0; k < W; ++k) xv[k] = cl[k] >= 0 ? __ldg(base + (size_t)cl[k] * n2_in) : 0.0;
+            }
+            const double* v = E.vals;
+            double a2 = 0.0;
+#pragma unroll
+            for (int k = 0; k < W; ++k)
+                if (cl[k] >= 0) a2 = fma(__ldg(v + (size_t)k * n1_out + r), xv[k], a2);
+            if (E.s_out == 0) acc0 = fma(E.scale, a2, acc0);
+            else acc1 = fma(E.scale, a2, acc1);
+        }
+        double* y0 = out + t;
+        double* y1 = out + per_s + t;
+        *y0 = beta == 0.0 ? acc0 : fma(beta, *y0, acc0);
+        *y1 = beta == 0.0 ? acc1 : fma(beta, *y1, acc1);
+    }
+}
+
 static int grid_for(int64_t total) {
     int64_t b = (total + 255) / 256;
     if (b > 148 * 64) b = 148 * 64;
@@ -163,6 +206,24 @@ int launch_gather(sg_problem* P, int dir, int W, int S_out, int64_t n1_in, int64
             if (el_in.e[e].s_out == s) el.e[el.ne++] = el_in.e[e];
     }
     for (int s = std::min(S_out, 2); s <= 2; ++s) el.sbeg[s] = el.ne;
+    if (dir == 0 && S_out == 2 && P->use_gather_s2 && n1_in * n2_in < (1LL << 31) && nrows_out * n2_in < (1LL << 31)) {
+        // sort by (input, s_in) so that entries sharing an input are adjacent
+        EntryList es;
+        es.ne = el_in.ne;
+        for (int e = 0; e < el_in.ne; ++e) es.e[e] = el_in.e[e];
+        std::stable_sort(es.e, es.e + es.ne, [](const Entry& a, const Entry& b) {
+            return a.in != b.in ? a.in < b.in : a.s_in < b.s_in;
+        });
+        es.sbeg[0] = es.sbeg[1] = es.sbeg[2] = 0;
+        const int g = grid_for(nrows_out * n2_in);
+#define GS2(WW) k_gather_s2<WW><<<g, 256, 0, P->stream>>>(n1_in, n2_in, nrows_out, cols, es, out, beta)
+        if (W == 3) GS2(3); else if (W == 7) GS2(7); else if (W == 15) GS2(15); else if (W == 2) GS2(2);
+        else return SG_ERR_ARG;
+#undef GS2
+        P->launches++;
+        SG_CUDA(cudaGetLastError());
+        return SG_OK;
+    }
     const int64_t n1_out = dir == 0 ? nrows_out : n1_in;
     const int64_t n2_out = dir == 1 ? nrows_out : n2_in;
     const int64_t total = (int64_t)S_out * n1_out * n2_out;

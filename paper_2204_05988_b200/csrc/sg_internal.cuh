@@ -245,7 +245,8 @@ struct sg_problem {
     bool use_cross_batched = true; // SG_NO_CROSS_BATCH disables
     int outer_mode = 0;            // 0 Richardson + minimal-residual safeguard, 1 plain Richardson, 2 MR always
     int64_t mr_switches = 0;
-    bool use_jobs2 = true;         // warp-unit transfer-job kernel (SG_OLD_JOBS: element kernel)
+    bool use_jobs2 = true;
+    bool use_gather_s2 = true;     // x-gather producing both dG(1) components per thread (SG_NO_GATHER_S2)         // warp-unit transfer-job kernel (SG_OLD_JOBS: element kernel)
     bool use_warm = true;          // warm-started block solves (SG_NO_WARM disables)
     bool warm_valid = false;
     bool use_vmom = true;          // moment pass 1 (SG_NO_VMOM disables)
