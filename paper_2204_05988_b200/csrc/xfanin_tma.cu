@@ -392,7 +392,7 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
     g_xft_minw = getenv("SG_XFT_MINW") ? atoi(getenv("SG_XFT_MINW")) : 4;
     // ... and small CTAs (one 2x2 line block x 4 column groups, 16 KB stages) beat larger tiles
     // on those lattices: more independent TMA producers per SM (grid (3,5): 2.02 -> 1.82 ms)
-    const int box_kb = getenv("SG_XFT_BOX_KB") ? P->xft_box_kb : (wc_auto ? 16 : 24);
+    const int box_kb = getenv("SG_XFT_BOX_KB") ? P->xft_box_kb : (wc_auto ? (d == 3 ? 16 : 8) : 24);
     XftTile tl = choose_tile(d, m, n2, P->xft_wc > 0 ? P->xft_wc : wc_auto, box_kb);
     if (tl.nw == 0) tl = choose_tile(d, m, n2, 0, 24);
     // split the sweep until there are >= 2 CTAs per SM
