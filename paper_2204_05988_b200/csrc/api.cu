@@ -83,6 +83,7 @@ extern "C" int sg_create(const sg_config* cfg, void* stream, sg_problem** out) {
     // strip) in round 1: opt-in
     P->use_jobs2 = getenv("SG_JOBS2") != nullptr;
     P->use_gather_s2 = getenv("SG_NO_GATHER_S2") == nullptr;
+    P->use_rbox = getenv("SG_NO_RBOX") == nullptr;
     // moment pass 1 (tables always prepared): used for d = 2 v-lattices, and for d = 3 only on
     // grids with a tiny x factor where the stored per-column coefficients outweigh the
     // intermediates (round-1 measurements, profiles/README.md); SG_VMOM forces it everywhere,

@@ -1219,6 +1219,114 @@ __global__ void __launch_bounds__(256) k_jobs2(JobList jl) {
     }
 }
 
+// Restriction (E^T) on a box lattice as a stencil: the coarse node c with
+// lattice coordinates z collects the fine node 2z (weight 1) and the midpoints 2z + delta of its
+// Kuhn edges (weight 1/2), delta in {0,1}^D u {0,-1}^D \ {0}; no pattern/value arrays are read.
+template <int D>
+__global__ void __launch_bounds__(256) k_jobs_rbox(JobList jl) {
+    int j = 0;
+    while (j + 1 < jl.nj && jl.j[j + 1].blk0 <= (int)blockIdx.x) ++j;
+    const Job& J = jl.j[j];
+    const unsigned n1_out = (unsigned)(J.dir == 0 ? J.nrows_out : J.n1_in);
+    const unsigned n2_out = (unsigned)(J.dir == 1 ? J.nrows_out : J.n2_in);
+    const unsigned per_s = n1_out * n2_out;
+    const unsigned total = per_s * (unsigned)J.S;
+    const unsigned n1i = (unsigned)J.n1_in, n2i = (unsigned)J.n2_in;
+    const int mf = J.box_mf, mc = (mf + 1) / 2;
+    const int nblk = (j + 1 < jl.nj ? jl.j[j + 1].blk0 : jl.total_blocks) - J.blk0;
+    for (unsigned t = (unsigned)(blockIdx.x - J.blk0) * blockDim.x + threadIdx.x; t < total;
+         t += (unsigned)nblk * blockDim.x) {
+        const unsigned s = t >= per_s ? 1u : 0u;
+        const unsigned rc = t - s * per_s;
+        const unsigned r = rc / n2_out, c = rc - r * n2_out;
+        unsigned node = J.dir == 1 ? c : r;   // coarse node
+        int z[D];
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+            z[q] = (int)(node % (unsigned)mc);
+            node /= (unsigned)mc;
+        }
+        int stride[D], fb = 0;
+        {
+            int st = 1;
+#pragma unroll
+            for (int q = 0; q < D; ++q) {
+                stride[q] = st;
+                fb += 2 * z[q] * st;
+                st *= mf;
+            }
+        }
+        const double* base = J.dir == 1 ? J.in + ((size_t)s * n1i + r) * n2i : J.in + (size_t)s * n1i * n2i + c;
+        const size_t fs = J.dir == 1 ? 1 : n2i;   // element stride of one fine node
+        double acc = base[(size_t)fb * fs];
+#pragma unroll
+        for (int sg = -1; sg <= 1; sg += 2)
+#pragma unroll
+            for (int mask = 1; mask < (1 << D); ++mask) {
+                bool ok = true;
+                int off = 0;
+#pragma unroll
+                for (int q = 0; q < D; ++q)
+                    if ((mask >> q) & 1) {
+                        const int fz = 2 * z[q] + sg;
+                        ok &= fz >= 0 && fz < mf;
+                        off += sg * stride[q];
+                    }
+                if (ok) acc = fma(0.5, __ldg(base + (size_t)(fb + off) * fs), acc);
+            }
+        const double v = (J.add ? J.add[t] : 0.0) + J.scale * acc;
+        if (J.opitch > 0)
+            J.out[((size_t)s * n1_out + r) * (size_t)J.opitch + c] = v;
+        else
+            J.out[t] = v;
+    }
+}
+
+// Prolongation (E) on a box lattice as a stencil: fine node f with lattice
+// parity pi = f mod 2 takes its coarse node f/2 (pi = 0) or the mean of the two ends (f -+ pi)/2
+// of the coarse Kuhn edge it bisects; no pattern/value arrays are read.
+template <int D>
+__global__ void __launch_bounds__(256) k_jobs_pbox(JobList jl) {
+    int j = 0;
+    while (j + 1 < jl.nj && jl.j[j + 1].blk0 <= (int)blockIdx.x) ++j;
+    const Job& J = jl.j[j];
+    const unsigned n1_out = (unsigned)(J.dir == 0 ? J.nrows_out : J.n1_in);
+    const unsigned n2_out = (unsigned)(J.dir == 1 ? J.nrows_out : J.n2_in);
+    const unsigned per_s = n1_out * n2_out;
+    const unsigned total = per_s * (unsigned)J.S;
+    const unsigned n1i = (unsigned)J.n1_in, n2i = (unsigned)J.n2_in;
+    const int mf = J.box_mf, mc = (mf + 1) / 2;
+    const int nblk = (j + 1 < jl.nj ? jl.j[j + 1].blk0 : jl.total_blocks) - J.blk0;
+    for (unsigned t = (unsigned)(blockIdx.x - J.blk0) * blockDim.x + threadIdx.x; t < total;
+         t += (unsigned)nblk * blockDim.x) {
+        const unsigned s = t >= per_s ? 1u : 0u;
+        const unsigned rc = t - s * per_s;
+        const unsigned r = rc / n2_out, c = rc - r * n2_out;
+        unsigned node = J.dir == 1 ? c : r;   // fine node
+        int lo = 0, hi = 0, st = 1;
+        bool mid = false;
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+            const int f = (int)(node % (unsigned)mf);
+            node /= (unsigned)mf;
+            const int pq = f & 1;
+            mid |= pq != 0;
+            lo += ((f - pq) >> 1) * st;
+            hi += ((f + pq) >> 1) * st;
+            st *= mc;
+        }
+        const double* base = J.dir == 1 ? J.in + ((size_t)s * n1i + r) * n2i : J.in + (size_t)s * n1i * n2i + c;
+        const size_t fs = J.dir == 1 ? 1 : n2i;
+        const double acc = mid ? 0.5 * __ldg(base + (size_t)lo * fs) + 0.5 * __ldg(base + (size_t)hi * fs)
+                               : __ldg(base + (size_t)lo * fs);
+        const double v = (J.add ? J.add[t] : 0.0) + J.scale * acc;
+        if (J.opitch > 0)
+            J.out[((size_t)s * n1_out + r) * (size_t)J.opitch + c] = v;
+        else
+            J.out[t] = v;
+    }
+}
+
 int launch_jobs(sg_problem* P, std::vector<Job>& jobs) {
     if (P->use_jobs2) {
         size_t i = 0;
@@ -1270,7 +1378,18 @@ int launch_jobs(sg_problem* P, std::vector<Job>& jobs) {
         }
         if (jl.nj == 0) continue;
         jl.total_blocks = blk;
-        k_jobs<<<blk, 256, 0, P->stream>>>(jl);
+        bool rbox = P->use_rbox;
+        for (int q = 0; q < jl.nj; ++q) rbox &= jl.j[q].box_mf > 0 && jl.j[q].W == jl.j[0].W;
+        const int dd = jl.j[0].W == 3 ? 1 : (jl.j[0].W == 7 ? 2 : (jl.j[0].W == 15 ? 3 : 0));
+        bool pbox = P->use_rbox;
+        for (int q = 0; q < jl.nj; ++q) pbox &= jl.j[q].box_mf > 0 && jl.j[q].W == 2 && jl.j[q].box_d == jl.j[0].box_d;
+        if (pbox && jl.j[0].box_d == 3) k_jobs_pbox<3><<<blk, 256, 0, P->stream>>>(jl);
+        else if (pbox && jl.j[0].box_d == 2) k_jobs_pbox<2><<<blk, 256, 0, P->stream>>>(jl);
+        else if (pbox && jl.j[0].box_d == 1) k_jobs_pbox<1><<<blk, 256, 0, P->stream>>>(jl);
+        else if (rbox && dd == 3) k_jobs_rbox<3><<<blk, 256, 0, P->stream>>>(jl);
+        else if (rbox && dd == 2) k_jobs_rbox<2><<<blk, 256, 0, P->stream>>>(jl);
+        else if (rbox && dd == 1) k_jobs_rbox<1><<<blk, 256, 0, P->stream>>>(jl);
+        else k_jobs<<<blk, 256, 0, P->stream>>>(jl);
         P->launches++;
         SG_CUDA(cudaGetLastError());
     }

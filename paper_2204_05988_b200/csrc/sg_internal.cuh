@@ -151,6 +151,8 @@ struct Job {
     double scale;
     int S, dir, W, blk0;
     int64_t opitch = 0;   // output row pitch (0: natural n2_out)
+    int box_mf = 0;       // transfer on a box lattice: fine lattice points per axis (0: use the ELL arrays)
+    int box_d = 0;        // ... and its dimension (prolongation jobs, W = 2)
 };
 struct JobList {
     int nj, total_blocks;
@@ -246,7 +248,8 @@ struct sg_problem {
     int outer_mode = 0;            // 0 Richardson + minimal-residual safeguard, 1 plain Richardson, 2 MR always
     int64_t mr_switches = 0;
     bool use_jobs2 = true;
-    bool use_gather_s2 = true;     // x-gather producing both dG(1) components per thread (SG_NO_GATHER_S2)         // warp-unit transfer-job kernel (SG_OLD_JOBS: element kernel)
+    bool use_gather_s2 = true;
+    bool use_rbox = true;          // stencil-form restriction jobs on box lattices (SG_NO_RBOX)     // x-gather producing both dG(1) components per thread (SG_NO_GATHER_S2)         // warp-unit transfer-job kernel (SG_OLD_JOBS: element kernel)
     bool use_warm = true;          // warm-started block solves (SG_NO_WARM disables)
     bool warm_valid = false;
     bool use_vmom = true;          // moment pass 1 (SG_NO_VMOM disables)

@@ -603,6 +603,7 @@ static int cross_lower_batched(sg_problem* P, const double* X, double* Y) {
                 const int lv0 = L - pp, lf = lv0 - k + 1, lc = lv0 - k;
                 jobs.push_back({Q(pp, k - 1), nullptr, Q(pp, k), P->fv.lev[lf].rcols, P->fv.lev[lf].rvals, n1(pp), n2(lf),
                                 n2(lc), 1.0, 1, 1, Wv, 0});
+                if (P->fv.kind == SG_MESH_BOX) jobs.back().box_mf = P->fv.lev[lf].m;
             }
             SG_TRY(launch_jobs(P, jobs));
         }
@@ -618,6 +619,8 @@ static int cross_lower_batched(sg_problem* P, const double* X, double* Y) {
                     J.out = H(p, o);
                     J.opitch = pit(lv);
                 }
+                J.box_mf = P->fx.lev[m].m;   // (box factor: checked by cross_lower_batched)
+                J.box_d = P->fx.d;
                 jobs.push_back(J);
             }
             SG_TRY(launch_jobs(P, jobs));
@@ -702,6 +705,7 @@ static int cross_upper_batched(sg_problem* P, const double* X, double* Y) {
                 const int lv = L - pp, lf = pp - k + 1, lc = pp - k;
                 jobs.push_back({Q(pp, k - 1), nullptr, Q(pp, k), P->fx.lev[lf].rcols, P->fx.lev[lf].rvals, n1(lf), n2(lv),
                                 n1(lc), 1.0, 1, 0, Wx, 0});
+                if (P->fx.kind == SG_MESH_BOX) jobs.back().box_mf = P->fx.lev[lf].m;
             }
             SG_TRY(launch_jobs(P, jobs));
         }
@@ -716,6 +720,8 @@ static int cross_upper_batched(sg_problem* P, const double* X, double* Y) {
                 double* out = (q == ng - p) ? H(p, a) : hb[q & 1] + A[p - 1].off1;
                 jobs.push_back({in, add, out, P->fv.lev[lvn].pcols, P->fv.lev[lvn].pvals, n1(p), n2(lvn - 1), n2(lvn), 1.0,
                                 1, 1, 2, 0});
+                jobs.back().box_mf = P->fv.lev[lvn].m;   // (box factor: checked by cross_upper_batched)
+                jobs.back().box_d = P->fv.d;
             }
             SG_TRY(launch_jobs(P, jobs));
         }
@@ -801,6 +807,7 @@ static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in
                 const int lv0 = L - pp, lf = lv0 - k + 1, lc = lv0 - k;
                 jobs.push_back({P->wsZ + qoff[pp - 1][k - 1], nullptr, P->wsZ + qoff[pp - 1][k], P->fv.lev[lf].rcols,
                                 P->fv.lev[lf].rvals, n1(pp), n2(lf), n2(lc), 1.0, S_in, 1, Wv, 0});
+                if (P->fv.kind == SG_MESH_BOX) jobs.back().box_mf = P->fv.lev[lf].m;
             }
             SG_TRY(launch_jobs(P, jobs));
         }
@@ -899,6 +906,7 @@ static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in
                     jobs.push_back({P->wsZ + qoff[pp - 1][k - 1], nullptr, P->wsZ + qoff[pp - 1][k],
                                     P->fx.lev[lf].rcols, P->fx.lev[lf].rvals, n1(lf), n2(lv), n1(lc), 1.0, S_in, 0, Wx,
                                     0});
+                    if (P->fx.kind == SG_MESH_BOX) jobs.back().box_mf = P->fx.lev[lf].m;
                 }
                 SG_TRY(launch_jobs(P, jobs));
             }
