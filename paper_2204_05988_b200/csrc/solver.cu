@@ -821,6 +821,10 @@ static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in
                 const double* in = m == 2 ? P->wsZ + qoff[0][p - 1] : hb[(m - 1) & 1] + offIn[p - 1];
                 jobs.push_back({in, P->wsZ + qoff[m - 1][p - m], hb[m & 1] + offIn[p - 1], P->fx.lev[m].pcols,
                                 P->fx.lev[m].pvals, n1(m - 1), n2(lv), n1(m), 1.0, S_in, 0, 2, 0});
+                if (P->fx.kind == SG_MESH_BOX) {
+                    jobs.back().box_mf = P->fx.lev[m].m;
+                    jobs.back().box_d = P->fx.d;
+                }
             }
             SG_TRY(launch_jobs(P, jobs));
         }
@@ -922,6 +926,10 @@ static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in
                     const double* add = pp > p ? P->wsZ + qoff[pp - 1][pp - p] : nullptr;
                     jobs.push_back({in, add, hb[q & 1] + offIn[p - 1], P->fv.lev[lvn].pcols, P->fv.lev[lvn].pvals, n1(p),
                                     n2(lvn - 1), n2(lvn), 1.0, S_in, 1, 2, 0});
+                    if (P->fv.kind == SG_MESH_BOX) {
+                        jobs.back().box_mf = P->fv.lev[lvn].m;
+                        jobs.back().box_d = P->fv.d;
+                    }
                 }
                 SG_TRY(launch_jobs(P, jobs));
             }
