@@ -361,3 +361,25 @@ def test_apply_strip_operator_full_size():
     expect = 512.0 + tau * 3 * 2 * 512.0
     val = float(Y.sum())
     assert abs(val - expect) <= 1e-12 * expect, (val, expect)
+
+
+def test_apply_strip_operator_full_size_4d():
+    """configs[2] at its full size (L=12, bench launch configuration): the balanced grid (6,6)
+    (17.9 M DOF, TMA pass 2 + moment pass 1) element by element against the oracle's exact
+    factor matrices on its own level-6 meshes."""
+    from oracle.sgrid import SGProblem
+    from paper_2204_05988_b200 import Problem
+    from oracle.problem import strip_terms
+    cfg = get_config("c2_4d_stream")
+    g = Problem(cfg)
+    gi = [i for i in range(g.num_grids(SET_ACTIVE)) if g.grid_info(SET_ACTIVE, i)[:2] == (6, 6)][0]
+    l1, l2, n1, n2 = g.grid_info(SET_ACTIVE, gi)
+    o = SGProblem(get_config("c2_4d_stream", L=7), galerkin="direct")   # meshes up to level 6
+    o.tau, o.delta = cfg["tau"], g.delta
+    o.terms = strip_terms(cfg, cfg["tau"], g.delta)
+    rng = np.random.default_rng(12)
+    X = rng.standard_normal((1, n1, n2))
+    Yt = torch.empty(n1 * n2, dtype=torch.float64, device="cuda")
+    g.sg_apply_strip_operator(SET_ACTIVE, gi, torch.from_numpy(X.ravel()).cuda(), Yt)
+    ref = o.apply_pair(o.terms, (6, 6), (6, 6), X)
+    assert relmax(Yt.cpu().numpy().reshape(X.shape), ref) <= 1e-12
