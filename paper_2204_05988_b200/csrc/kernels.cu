@@ -920,7 +920,8 @@ int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const St
     const int64_t nrows = (int64_t)S * n1;
     const int64_t ctiles = (n2 + VF_TC - 1) / VF_TC;
     // enough blocks to fill the machine, as many rows per block as possible (coefficient reuse)
-    int64_t rchunks = std::max<int64_t>(1, (148 * 6 + ctiles - 1) / ctiles);
+    static const int vf_mult = getenv("SG_VF_BLK") ? atoi(getenv("SG_VF_BLK")) : 12;   // 12 per SM measured best
+    int64_t rchunks = std::max<int64_t>(1, (148 * vf_mult + ctiles - 1) / ctiles);
     rchunks = std::min<int64_t>(rchunks, (nrows + 15) / 16);
     rchunks = std::max<int64_t>(rchunks, 1);
     const int64_t rpb = (nrows + rchunks - 1) / rchunks;
