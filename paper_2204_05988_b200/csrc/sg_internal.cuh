@@ -232,7 +232,8 @@ struct sg_problem {
     int xfi_cpt = 1, xfi_seg = 0;
     bool use_xfi_tma = true;
     int xft_wc = 0, xft_box_kb = 24;   // TMA tile: forced column groups (SG_XFT_WC), stage box limit (SG_XFT_BOX_KB)
-    int xft_smem_kb = 0;           // shared-memory budget of the TMA pipeline (SG_XFT_SMEM_KB; 0: 4 stages)
+    int xft_smem_kb = 0;
+    int xft_nst_wide = 3;          // pipeline depth of the wide-box 3D tiles (SG_XFT_NST_WIDE)           // shared-memory budget of the TMA pipeline (SG_XFT_SMEM_KB; 0: 4 stages)
     bool use_xwhole = true;        // whole-x pass 2 on tiny x lattices (SG_NO_XWHOLE disables)       // TMA-pipelined pass 2 (SG_NO_TMA disables)  // SG_XFI_CPT (columns per lane), SG_XFI_SEG (sweep segment length, 0 auto)
     std::vector<double*> xfi_itab; // per x-level: interior groups only [3^d][ng_int][W]
     std::vector<double*> xfi_tab;  // per x-level: class table [3^d][groups][W] of the combined x matrices

@@ -437,7 +437,7 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
     const size_t stage_b = (size_t)tl.e1 * tl.e2 * tl.bc * 8;
     // 4 stages measured best (deeper rings shrink L1 and were slower: (2,6) 3.3 -> 5.1 ms at 8 stages)
     tl.nst = P->xft_smem_kb > 0 ? (int)std::min<size_t>(XFT_MAXST, std::max<size_t>(2, (size_t)(P->xft_smem_kb * 1024) / stage_b))
-                                : 4;
+                                : (wc_auto && d == 3 ? P->xft_nst_wide : 4);
     const size_t smem = (size_t)tl.nst * stage_b + 2 * tl.nst * sizeof(uint64_t);
     {
         int ncls = 1;
