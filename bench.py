@@ -96,6 +96,15 @@ def peaks():
         return {}
 
 
+def apply_traffic(workload):
+    """Measured DRAM bytes per DOF-apply of the strip-operator apply for this workload,
+    from the committed ncu capture (tools/apply_traffic.py -> profiles/apply_traffic.json)."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "apply_traffic.json")))[workload]
+    except Exception:
+        return None
+
+
 def combine_ranks(ms, dof, world, device="cpu"):
     """Replicas-only aggregation: time = max over ranks,
     work = sum over ranks.  Host logic, tested with gloo on CPU."""
@@ -255,6 +264,14 @@ def main():
             "traffic_note": "per-launch DRAM bytes from ncu --set full in profiles/ (per grid)",
             "share_of_step": (kt["ms"] / ms) if ms > 0 else None,
             "avg_apply_ms": kt["ms"] / max(st["applies"], 1)}
+    tr = apply_traffic(cfg["name"])
+    if tr and st["applies"]:
+        dof_per_apply = float(st["dof_applied"]) / st["applies"]
+        roof["traffic"] = tr["dram_bytes_per_dof"] * dof_per_apply
+        roof["traffic_note"] = ("ncu dram__bytes_read.sum + dram__bytes_write.sum of the apply kernels, "
+                                "%.1f B per DOF-apply (%s) x %.0f DOF per apply of this run; algorithmic: %.1f B"
+                                % (tr["dram_bytes_per_dof"], tr["source"], dof_per_apply,
+                                   kt["bytes"] / max(kt["launches"], 1)))
     clocks = clk.summary()
     out = {"metric": METRIC, "value": value, "unit": "DOF-applies/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
