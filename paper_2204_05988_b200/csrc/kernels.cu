@@ -338,8 +338,8 @@ int launch_ell_to_stencil(sg_problem* P, int64_t n, int W, const int32_t* cols, 
 // index >= ng_int are only needed on x-boundary rows (face terms).
 constexpr int VF_TC = 32;   // columns per block
 constexpr int VF_RL = 8;    // row lanes per block
-template <int D, int R>
-__global__ void __launch_bounds__(VF_TC * VF_RL, 2) k_vfan_st(int64_t nrows, int64_t n1, int64_t n2, StencilOff so,
+template <int D, int R, int MINB = 2>
+__global__ void __launch_bounds__(VF_TC * VF_RL, MINB) k_vfan_st(int64_t nrows, int64_t n1, int64_t n2, StencilOff so,
                                                               const uint8_t* __restrict__ xflag, VfanParams vp,
                                                               const double* __restrict__ X, int64_t rows_per_block,
                                                               int64_t opitch) {
@@ -355,11 +355,11 @@ __global__ void __launch_bounds__(VF_TC * VF_RL, 2) k_vfan_st(int64_t nrows, int
         sm[idx] = ac < n2 ? __ldg(vp.vst[g] + k * n2 + ac) : 0.0;
     }
     __syncthreads();
-    int64_t addr[W];
+    int32_t addr[W];   // column offsets within a row (n2 < 2^31)
 #pragma unroll
     for (int k = 0; k < W; ++k) {
         int64_t c = a + so.off[k];
-        addr[k] = c < 0 ? 0 : (c >= n2 ? n2 - 1 : c);
+        addr[k] = (int32_t)(c < 0 ? 0 : (c >= n2 ? n2 - 1 : c));
     }
     const int64_t rb = blockIdx.y * rows_per_block;
     const int64_t re = min(nrows, rb + rows_per_block);
@@ -934,8 +934,19 @@ int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const St
         cudaFuncSetAttribute(k_vfan_st<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k_vfan_st<2, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch);
     } else {
-        cudaFuncSetAttribute(k_vfan_st<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_vfan_st<3, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch);
+        // rows per thread on 3D v-lattices (SG_VF_R = 3/4: more coefficient reuse per shared load,
+        // one resident block of registers per thread pair)
+        const int vf_r = getenv("SG_VF_R") ? atoi(getenv("SG_VF_R")) : 2;
+        if (vf_r == 4) {
+            cudaFuncSetAttribute(k_vfan_st<3, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_vfan_st<3, 4, 1><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch);
+        } else if (vf_r == 3) {
+            cudaFuncSetAttribute(k_vfan_st<3, 3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_vfan_st<3, 3, 1><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch);
+        } else {
+            cudaFuncSetAttribute(k_vfan_st<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_vfan_st<3, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch);
+        }
     }
     P->launches++;
     SG_CUDA(cudaGetLastError());

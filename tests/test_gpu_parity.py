@@ -295,7 +295,8 @@ def test_zero_rhs_gives_zero():
 
 
 @pytest.mark.parametrize("env", ["SG_FUSED", "SG_FORCE_XFIRST", "SG_BRICK", "SG_REG", "SG_OLD_XG",
-                                 "SG_XFI_SEG=1", "SG_XFI_SEG=3", "SG_XFI_CPT=2", "SG_NO_TMA", "SG_NO_XWHOLE", "SG_NO_VMOM", "SG_VMOM", "SG_NO_CROSS_BATCH", "SG_VFANK", "SG_NO_GATHER_S2", "SG_NO_RBOX"])
+                                 "SG_XFI_SEG=1", "SG_XFI_SEG=3", "SG_XFI_CPT=2", "SG_NO_TMA", "SG_NO_XWHOLE", "SG_NO_VMOM", "SG_VMOM", "SG_NO_CROSS_BATCH", "SG_VFANK", "SG_NO_GATHER_S2", "SG_NO_RBOX",
+                                 "SG_VF_R=2", "SG_VF_R=3", "SG_VF_R=4"])
 @pytest.mark.parametrize("name", CONFIG_ORDER)
 def test_apply_strip_operator_kernel_paths(name, env, monkeypatch):
     """Same parity on every kernel path at test sizes: the opt-in fused whole-x

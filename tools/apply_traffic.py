@@ -4,7 +4,8 @@ Input: the CSV of
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv \
       python tools/apply_bench.py --config C --reps 1
 which runs 1 + reps applies on every active grid.  Only the library's own kernels
-(namespace sg::) are counted; torch's randn/empty kernels are dropped.
+(namespace sg::) after the first torch randn launch are counted: the mesh/assembly
+setup before it and torch's own kernels are dropped.
 
 Usage: apply_traffic.py CSV CONFIG TOTAL_DOF APPLIES_PER_GRID OUT_JSON
 TOTAL_DOF = sum of S*n1*n2 over the grids (apply_bench's last line).  The result
@@ -22,8 +23,13 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1
          "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3}
 per = defaultdict(dict)
 names = {}
+started = False
 for r in rows[start + 1:]:
-    if len(r) <= vi or "sg::" not in r[ni]:
+    if len(r) <= vi:
+        continue
+    if "distribution" in r[ni]:
+        started = True
+    if not started or "sg::" not in r[ni]:
         continue
     try:
         v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
