@@ -180,7 +180,8 @@ class SGProblem:
         combined by the combination formula ("for interpolation
         such a scheme ... gives the exact result").  Reading R8: this
         is how the initial value u0 (eq. (4), U_0^- = u0) enters; it reproduces
-        PAPER.md Table 1 (l.597-628) to within 10% (tests/test_oracle_paper.py)."""
+        PAPER.md Table 1 (l.597-628) to within 10% (tests/test_oracle_sgrid.py::
+        test_paper_table1_d1_r1)."""
         vals = {}
         for l in self.active + self.coarse:
             mx, mv = self.Hx.meshes[l[0]], self.Hv.meshes[l[1]]

@@ -95,7 +95,8 @@ def test_solution_satisfies_galerkin_system():
 
 
 def test_paper_table1_d1_r1():
-    """Golden: PAPER.md Table 1 (l.597-628), d=1, r=1, L=2..4 within 10% (SPEC asks factor 2)."""
+    """Golden: PAPER.md Table 1 (l.597-628), d=1, r=1, L=2..4 within 10% (SPEC asks factor 2;
+    measured deviations 1-6 %, reading R8)."""
     gold = json.load(open(os.path.join(GOLD, "paper_table1_d1_r1.json")))
     for Lp in (2, 3, 4):
         cfg = dict(name="table1", d=1, xmesh=dict(kind="periodic", lo=[0.0], hi=[1.0]),
@@ -119,7 +120,7 @@ def test_paper_table1_d1_r1():
                 e2 += np.sum(W * (Ui - E) ** 2); n2 += np.sum(W * E ** 2)
         rel = math.sqrt(e2 / n2)
         ref = gold["rel_err"][Lp - 1]
-        assert 0.8 * ref <= rel <= 1.2 * ref, (Lp, rel, ref)
+        assert 0.9 * ref <= rel <= 1.1 * ref, (Lp, rel, ref)
 
 
 def test_convergence_rate_vs_characteristics():
