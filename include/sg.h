@@ -27,6 +27,9 @@
  *    unless a function says "host or device"; they must not alias unless
  *    stated.  All work is enqueued on the handle's stream (sg_create); calls
  *    returning values computed on the device synchronise that stream.
+ *    Handles that share a device must share that stream (or be serialised by
+ *    the caller): the pass-2 kernels stage their per-level coefficient tables
+ *    in the module's constant bank right before each launch.
  *  - Errors: functions return SG_OK (0) or an SG_ERR_* code; sg_last_error()
  *    returns a thread-local message.  After SG_ERR_CUDA the handle must be
  *    destroyed.
@@ -45,6 +48,7 @@ extern "C" {
 #define SG_ERR_CUDA 2
 #define SG_ERR_STATE 3
 #define SG_ERR_UNSUPPORTED 4
+#define SG_ERR_NOCONV 5   /* iteration limit reached before the tolerance (result still written) */
 
 #define SG_MESH_BOX 0
 #define SG_MESH_LSHAPE 1 /* [-1,1]^2 minus the open quadrant {x>0, y<0} */
@@ -162,29 +166,47 @@ int sg_interp_u0(sg_problem* P, double* u);
 /* right-hand side of strip j >= 1 (eq. (4)): jump load from trace_prev (active
  * spatial vector U_{j-1}^-) plus the inflow load (cfg.inflow).  b: active (S). */
 int sg_rhs(sg_problem* P, int j, const double* trace_prev, double* b);
-/* Richardson with the combination preconditioner (l.540-566) on the device.
- * b, u: active (S) vectors; u is used as initial guess (zero it for the
- * paper's u^(0) = 0).  Stops when ||du||_{L2(I_j x Omega)} <= rtol*||u||.
- * Inner block solves (15): BiCGStab to relative residual inner_rtol. */
+/* Richardson with the combination preconditioner (l.540-566), entirely on the device
+ * (one CUDA graph with conditional nodes; the only host synchronisation is at the end).
+ * b, u: active (S) vectors; u is used as initial guess (zero it for the paper's
+ * u^(0) = 0).  du = P^{-1} r is the preconditioned residual; the step is u -= omega du
+ * with omega = 1 (the paper) or, after the safeguard of reading R13 engaged, the
+ * residual-minimising omega.  Stops when ||du||_{L2(I_j x Omega)} <= rtol*||u||.
+ * Inner block solves (15): BiCGStab to relative residual inner_rtol (cap 500).
+ * Returns SG_ERR_NOCONV when max_iter iterations did not reach rtol (u, iters and
+ * last_norm are still written), SG_ERR_STATE on a non-finite update. */
 int sg_solve_strip(sg_problem* P, const double* b, double* u, double rtol, double inner_rtol, int max_iter,
                    int* iters, double* last_norm);
 /* nsteps strips starting at strip j0 >= 1: trace (active spatial vector,
- * HOST or DEVICE) holds U_{j0-1}^- on entry and U_{j0+nsteps-1}^- on exit. */
+ * HOST or DEVICE) holds U_{j0-1}^- on entry and U_{j0+nsteps-1}^- on exit.
+ * The strips are enqueued back to back (max_iter 200 each) and the handle's stream is
+ * synchronised once at the end; SG_ERR_NOCONV if any strip solve hit max_iter. */
 int sg_step(sg_problem* P, int j0, int nsteps, double* trace, double rtol, double inner_rtol);
 
 /* ---- instrumentation ----------------------------------------------------- */
-/* counters since the last reset: strip-operator applies, DOFs applied, our
- * kernel launches, Richardson and inner iterations */
-int sg_stats(const sg_problem* P, int64_t* n_applies, int64_t* dof_applied, int64_t* launches,
+/* Counters since the last reset (synchronises the handle's stream): strip-operator
+ * applies and DOFs applied (the block solves of the strip solver count on the device,
+ * applies issued through sg_apply_strip_operator on the host), our kernel launches
+ * (graph executions are expanded to the kernels they ran), Richardson and inner
+ * (BiCGStab) iterations. */
+int sg_stats(sg_problem* P, int64_t* n_applies, int64_t* dof_applied, int64_t* launches,
              int64_t* outer_iters, int64_t* inner_iters);
+/* Solver health since the last reset: strip solves that stopped at max_iter, solves
+ * stopped by a non-finite update, inner block solves that stopped at their iteration
+ * cap, inner BiCGStab breakdowns (a grid's rho or omega became 0 / non-finite; the grid
+ * keeps its last iterate).  A bench line with non-zero counts is flagged. */
+int sg_solver_health(sg_problem* P, int64_t* outer_unconverged, int64_t* outer_nonfinite, int64_t* inner_maxit,
+                     int64_t* inner_breakdowns);
 int sg_reset_stats(sg_problem* P);
 /* number of strip solves (since the last reset) in which the outer Richardson
  * iteration switched to residual-minimising step lengths because the update
  * norm grew (safeguard, reading R13); SG_OUTER=1 disables it */
-int sg_outer_switches(const sg_problem* P, int64_t* switches);
-/* when on, CUDA events bracket every launch of the strip-operator kernels;
- * sg_kernel_time returns their summed device time (ms), launch count and
- * algorithmic bytes (read X + write Y + factor matrices) */
+int sg_outer_switches(sg_problem* P, int64_t* switches);
+/* Timing mode: device timestamps (globaltimer, in the captured graphs too) bracket every
+ * strip-operator apply; sg_kernel_time returns the summed device time (ms) of the applies
+ * that did work (converged grids excluded), their count, their algorithmic bytes (read X +
+ * write Y + the factor data the launched kernels read) and algorithmic FLOPs (2 per
+ * multiply-add on the structural nonzeros of the factor matrices). */
 int sg_set_timing(sg_problem* P, int on);
 int sg_kernel_time(sg_problem* P, double* ms, int64_t* launches, double* alg_bytes, double* alg_flops);
 

@@ -18,6 +18,13 @@ class SGError(RuntimeError):
     pass
 
 
+class SGNoConvergence(SGError):
+    """SG_ERR_NOCONV: an iteration limit was reached before the tolerance (results are written)."""
+
+
+SG_ERR_NOCONV = 5
+
+
 def lib_path() -> str:
     return os.path.join(_HERE, "libsg.so")
 
@@ -83,6 +90,7 @@ def load_library():
         "sg_solve_strip": (I, [P, P, P, D, D, I, pI, pD]),
         "sg_step": (I, [P, I, I, P, D, D]),
         "sg_stats": (I, [P, pI64, pI64, pI64, pI64, pI64]),
+        "sg_solver_health": (I, [P, pI64, pI64, pI64, pI64]),
         "sg_outer_switches": (I, [P, pI64]),
         "sg_reset_stats": (I, [P]),
         "sg_set_timing": (I, [P, I]),
@@ -97,6 +105,8 @@ def load_library():
 
 
 def _check(rc):
+    if rc == SG_ERR_NOCONV:
+        raise SGNoConvergence(f"libsg: {_LIB.sg_last_error().decode()}")
     if rc != 0:
         raise SGError(f"libsg error {rc}: {_LIB.sg_last_error().decode()}")
 
@@ -148,10 +158,15 @@ def config_from_dict(cfg: dict) -> sg_config:
     return c
 
 
-def _ptr(t):
-    """Device pointer of a torch CUDA tensor (fp64, contiguous)."""
+def _ptr(t, n=None, name="buffer"):
+    """Device pointer of a torch CUDA tensor (fp64, contiguous, at least n elements)."""
     import torch
-    assert isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
+    if not (isinstance(t, torch.Tensor) and t.is_cuda):
+        raise SGError(f"{name}: expected a torch CUDA tensor")
+    if t.dtype != torch.float64 or not t.is_contiguous():
+        raise SGError(f"{name}: expected a contiguous float64 tensor")
+    if n is not None and t.numel() < n:
+        raise SGError(f"{name}: {t.numel()} elements, the call needs {n}")
     return C.c_void_p(t.data_ptr())
 
 
@@ -254,47 +269,72 @@ class Problem:
         _check(self.lib.sg_factor_export(self.h, factor, spec, level, vals.ctypes.data_as(C.c_void_p)))
         return vals
 
-    # hot path
+    # hot path (buffer sizes are checked against the handle's layout before any call)
+    def _na(self, S=None):
+        return self.set_size(SG_SET_ACTIVE, self.S if S is None else S)
+
     def sg_apply_strip_operator(self, set_, g, X, Y):
-        _check(self.lib.sg_apply_strip_operator(self.h, set_, g, _ptr(X), _ptr(Y)))
+        _, _, n1, n2 = self.grid_info(set_, g)
+        n = self.S * n1 * n2
+        _check(self.lib.sg_apply_strip_operator(self.h, set_, g, _ptr(X, n, "X"), _ptr(Y, n, "Y")))
 
     def sg_apply_full(self, X, Y):
-        _check(self.lib.sg_apply_full(self.h, _ptr(X), _ptr(Y)))
+        n = self._na()
+        _check(self.lib.sg_apply_full(self.h, _ptr(X, n, "X"), _ptr(Y, n, "Y")))
 
     def sg_apply_mass_full(self, Tb, X, Y):
         Tb = np.ascontiguousarray(Tb, dtype=np.float64)
+        if Tb.ndim != 2:
+            raise SGError("Tb: expected a 2D (S_out x S_in) array")
         _check(self.lib.sg_apply_mass_full(self.h, Tb.ctypes.data_as(C.POINTER(C.c_double)), Tb.shape[0],
-                                           Tb.shape[1], _ptr(X), _ptr(Y)))
+                                           Tb.shape[1], _ptr(X, self._na(Tb.shape[1]), "X"),
+                                           _ptr(Y, self._na(Tb.shape[0]), "Y")))
+
+    def _transfer_sizes(self, factor, lf, lc, level_other, S):
+        nf, _, _ = self.mesh_info(factor, lf)
+        nc, _, _ = self.mesh_info(factor, lc)
+        no, _, _ = self.mesh_info(1 - factor, level_other)
+        return S * nc * no, S * nf * no
 
     def sg_prolongate(self, factor, lf, lc, level_other, S, inp, out, beta=0.0):
-        _check(self.lib.sg_prolongate(self.h, factor, lf, lc, level_other, S, _ptr(inp), _ptr(out), beta))
+        ncoarse, nfine = self._transfer_sizes(factor, lf, lc, level_other, S)
+        _check(self.lib.sg_prolongate(self.h, factor, lf, lc, level_other, S, _ptr(inp, ncoarse, "in"),
+                                      _ptr(out, nfine, "out"), beta))
 
     def sg_restrict(self, factor, lc, lf, level_other, S, inp, out, beta=0.0):
-        _check(self.lib.sg_restrict(self.h, factor, lc, lf, level_other, S, _ptr(inp), _ptr(out), beta))
+        ncoarse, nfine = self._transfer_sizes(factor, lf, lc, level_other, S)
+        _check(self.lib.sg_restrict(self.h, factor, lc, lf, level_other, S, _ptr(inp, nfine, "in"),
+                                    _ptr(out, ncoarse, "out"), beta))
 
     def sg_combine(self, dhat_active, dhat_coarse, du):
-        _check(self.lib.sg_combine(self.h, _ptr(dhat_active), _ptr(dhat_coarse) if dhat_coarse is not None
-                                   else C.c_void_p(0), _ptr(du)))
+        nc = self.set_size(SG_SET_COARSE, self.S)
+        _check(self.lib.sg_combine(self.h, _ptr(dhat_active, self._na(), "dhat_active"),
+                                   _ptr(dhat_coarse, nc, "dhat_coarse") if dhat_coarse is not None
+                                   else C.c_void_p(0), _ptr(du, self._na(), "du")))
 
     def sg_interp_u0(self, u):
-        _check(self.lib.sg_interp_u0(self.h, _ptr(u)))
+        _check(self.lib.sg_interp_u0(self.h, _ptr(u, self._na(1), "u")))
 
     def sg_rhs(self, j, trace_prev, b):
-        _check(self.lib.sg_rhs(self.h, j, _ptr(trace_prev), _ptr(b)))
+        _check(self.lib.sg_rhs(self.h, j, _ptr(trace_prev, self._na(1), "trace_prev"), _ptr(b, self._na(), "b")))
 
     def sg_solve_strip(self, b, u, rtol=1e-12, inner_rtol=1e-12, max_iter=200):
+        """Returns (iterations, last update norm); raises SGNoConvergence at max_iter."""
         it, last = C.c_int(), C.c_double()
-        _check(self.lib.sg_solve_strip(self.h, _ptr(b), _ptr(u), rtol, inner_rtol, max_iter, C.byref(it),
-                                       C.byref(last)))
+        n = self._na()
+        _check(self.lib.sg_solve_strip(self.h, _ptr(b, n, "b"), _ptr(u, n, "u"), rtol, inner_rtol, max_iter,
+                                       C.byref(it), C.byref(last)))
         return it.value, last.value
 
     def sg_step(self, j0, nsteps, trace, rtol=1e-10, inner_rtol=1e-10):
         """trace: torch CUDA tensor or numpy array (host); updated in place."""
+        n = self._na(1)
         if isinstance(trace, np.ndarray):
-            assert trace.dtype == np.float64 and trace.flags["C_CONTIGUOUS"]
+            if trace.dtype != np.float64 or not trace.flags["C_CONTIGUOUS"] or trace.size < n:
+                raise SGError(f"trace: expected a contiguous float64 array of >= {n} elements")
             p = trace.ctypes.data_as(C.c_void_p)
         else:
-            p = _ptr(trace)
+            p = _ptr(trace, n, "trace")
         _check(self.lib.sg_step(self.h, j0, nsteps, p, rtol, inner_rtol))
 
     # instrumentation
@@ -305,6 +345,12 @@ class Problem:
         _check(self.lib.sg_outer_switches(self.h, C.byref(sw)))
         return dict(zip(["applies", "dof_applied", "launches", "outer_iters", "inner_iters", "outer_mr_switches"],
                         [x.value for x in v] + [sw.value]))
+
+    def health(self):
+        v = [C.c_int64() for _ in range(4)]
+        _check(self.lib.sg_solver_health(self.h, *[C.byref(x) for x in v]))
+        return dict(zip(["outer_unconverged", "outer_nonfinite", "inner_maxit", "inner_breakdowns"],
+                        [x.value for x in v]))
 
     def reset_stats(self):
         _check(self.lib.sg_reset_stats(self.h))

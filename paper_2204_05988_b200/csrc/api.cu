@@ -11,12 +11,6 @@ namespace sg {
 const char* last_error();
 int expand_terms(sg_problem* P);
 int combine_group(sg_problem* P, Group& g, bool other_is_x);
-int combine(sg_problem* P, int S, const double* dhat_a, const double* dhat_c, double* du);
-int interp_u0(sg_problem* P, double* u);
-int rhs(sg_problem* P, int j, const double* trace, double* b);
-int solve_strip(sg_problem* P, const double* b, double* u, double rtol, double inner_rtol, int max_iter, int* iters,
-                double* last);
-int step(sg_problem* P, int j0, int nsteps, double* trace_dev, double rtol, double inner_rtol);
 }  // namespace sg
 
 using namespace sg;
@@ -59,40 +53,13 @@ extern "C" int sg_create(const sg_config* cfg, void* stream, sg_problem** out) {
     P->cfg = *cfg;
     P->stream = (cudaStream_t)stream;
     P->verbose = getenv("SG_VERBOSE") != nullptr;
-    P->use_classes = getenv("SG_NO_CLASSES") == nullptr;
-    // the fused whole-x kernel is instruction bound (one load per FMA) and slower than the
-    // two-pass kernels on B200 in round-1 measurements: opt-in only
-    P->use_fused = getenv("SG_FUSED") != nullptr;
     P->use_graphs = getenv("SG_NO_GRAPHS") == nullptr;
-    P->use_reg = getenv("SG_REG") != nullptr;   // measured slower in round 1: opt-in
-    P->use_brick = getenv("SG_BRICK") != nullptr;   // measured 4x slower in round 1: opt-in
-    P->use_xfanin = getenv("SG_OLD_XG") == nullptr;
-    P->use_xfi_tma = getenv("SG_NO_TMA") == nullptr;
-    P->xft_nst_wide = getenv("SG_XFT_NST_WIDE") ? atoi(getenv("SG_XFT_NST_WIDE")) : 3;   // measured: 3 stages 1.2% faster
-    P->xft_wc = getenv("SG_XFT_WC") ? atoi(getenv("SG_XFT_WC")) : 0;
-    P->xft_box_kb = getenv("SG_XFT_BOX_KB") ? atoi(getenv("SG_XFT_BOX_KB")) : 24;
-    P->xft_smem_kb = getenv("SG_XFT_SMEM_KB") ? atoi(getenv("SG_XFT_SMEM_KB")) : 0;   // 0: 4 stages
-    P->use_xwhole = getenv("SG_NO_XWHOLE") == nullptr;
+    // fallback of the TMA line sweep (register line sweep k_xfanin)
+    P->use_tma = getenv("SG_NO_TMA") == nullptr;
+    // fallback of the batched cross-grid lower part (also taken when its buffers do not fit)
     P->use_cross_batched = getenv("SG_NO_CROSS_BATCH") == nullptr;
+    // outer step length (reading R13): 0 Richardson + MR safeguard, 1 plain, 2 MR always
     P->outer_mode = getenv("SG_OUTER") ? atoi(getenv("SG_OUTER")) : 0;
-    // k-outer pass-1 kernel: more rows per coefficient load but register-starved; measured slower
-    // than k_vfan_st on both 3D (1.35-1.86 vs 0.85 ms on grid (4,4)) in round 1: opt-in
-    P->use_vfan_k = getenv("SG_VFANK") != nullptr;
-    // warm-started block solves: measured no gain (configs[4]: 535 vs 526 inner its), opt-in
-    P->use_warm = getenv("SG_WARM") != nullptr;
-    // warp-unit transfer jobs: measured slower than the element kernel (7.3 vs 2.6 s per configs[4]
-    // strip) in round 1: opt-in
-    P->use_jobs2 = getenv("SG_JOBS2") != nullptr;
-    P->use_gather_s2 = getenv("SG_NO_GATHER_S2") == nullptr;
-    P->use_rbox = getenv("SG_NO_RBOX") == nullptr;
-    // moment pass 1 (tables always prepared): used for d = 2 v-lattices, and for d = 3 only on
-    // grids with a tiny x factor where the stored per-column coefficients outweigh the
-    // intermediates (round-1 measurements, profiles/README.md); SG_VMOM forces it everywhere,
-    // SG_NO_VMOM off
-    P->use_vmom = getenv("SG_NO_VMOM") == nullptr;
-    P->force_vmom = getenv("SG_VMOM") != nullptr;
-    P->xfi_cpt = getenv("SG_XFI_CPT") ? atoi(getenv("SG_XFI_CPT")) : 1;
-    P->xfi_seg = getenv("SG_XFI_SEG") ? atoi(getenv("SG_XFI_SEG")) : 0;
     if (cudaStreamCreateWithFlags(&P->gstream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&P->ev_a, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&P->ev_b, cudaEventDisableTiming) != cudaSuccess) {
@@ -100,9 +67,6 @@ extern "C" int sg_create(const sg_config* cfg, void* stream, sg_problem** out) {
         delete P;
         return SG_ERR_CUDA;
     }
-    // x-first for n1 > n2 measured slower than v-first on configs[4] (19 vs 10 intermediates):
-    // never by default, SG_XFIRST_AUTO / SG_FORCE_XFIRST opt in
-    P->xfirst_mode = getenv("SG_FORCE_XFIRST") ? 2 : (getenv("SG_XFIRST_AUTO") ? 0 : 1);
     P->S = cfg->q + 1;
     P->F = cfg->L - 1;
     auto setf = [&](Factor& f, int kind, const double* lo, const double* hi) {
@@ -209,17 +173,19 @@ extern "C" int sg_assemble_factors(sg_problem* P) {
     SG_CUDA(cudaMalloc(&P->red, sizeof(double) * 3 * nblk));
     SG_CUDA(cudaMalloc(&P->scal, sizeof(double) * 10 * (MAX_SEG + 1)));
     SG_CUDA(cudaMemset(P->scal, 0, sizeof(double) * 10 * (MAX_SEG + 1)));
-    SG_CUDA(cudaMallocHost(&P->hscal, sizeof(double) * 10 * (MAX_SEG + 1)));
     const int64_t nF = std::max(P->fx.lev[F].n, P->fv.lev[F].n) + 16;
     const int64_t sizes[17] = {Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na + Nc, Na, Na + Nc, Na + Nc, Na,
                                std::max(Na, 4 * nF), Na, Na, Na + Nc, Na + Nc, Na, Na + Nc};
     P->vec.assign(17, nullptr);
     for (int i = 0; i < 17; ++i) SG_CUDA(cudaMalloc(&P->vec[i], sizeof(double) * sizes[i]));
-    P->use_precond = getenv("SG_NO_PRECOND") == nullptr;
     SG_TRY(build_block_jacobi(P));
+    SG_TRY(count_nnz(P));
+    SG_TRY(solver_init(P));
     SG_CUDA(cudaMalloc(&P->trace_dev, sizeof(double) * set_size(P, SG_SET_ACTIVE, 1)));
     SG_CUDA(cudaStreamSynchronize(P->stream));
     P->assembled = true;
+    // buffers of the batched cross-grid apply (allocated here, never inside a graph capture)
+    SG_TRY(apply_cross_prepare(P));
     return SG_OK;
 }
 
@@ -251,19 +217,14 @@ extern "C" void sg_destroy(sg_problem* P) {
     for (double* t : P->vm_tab) cudaFree(t);
     for (double* t : P->xw_dev) cudaFree(t);
     for (int* t : P->vm_blist) cudaFree(t);
-    if (P->hscal) cudaFreeHost(P->hscal);
+    solver_destroy(P);
     for (double* v : P->vec) cudaFree(v);
     cudaFree(P->trace_dev);
     cudaFree(P->dinv);
-    cudaFree(P->egrp_dev);
     for (auto& g : P->graphs) cudaGraphExecDestroy(g.exec);
     if (P->gstream) cudaStreamDestroy(P->gstream);
     if (P->ev_a) cudaEventDestroy(P->ev_a);
     if (P->ev_b) cudaEventDestroy(P->ev_b);
-    for (auto& pr : P->ev_pairs) {
-        cudaEventDestroy(pr.first);
-        cudaEventDestroy(pr.second);
-    }
     delete P;
 }
 
@@ -487,30 +448,34 @@ extern "C" int sg_step(sg_problem* P, int j0, int nsteps, double* trace, double 
 }
 
 // ---------------------------------------------------------- instrumentation
-extern "C" int sg_stats(const sg_problem* P, int64_t* n_applies, int64_t* dof_applied, int64_t* launches,
+// host counters (applies issued directly through the ABI) + device counters (strip solver)
+extern "C" int sg_stats(sg_problem* P, int64_t* n_applies, int64_t* dof_applied, int64_t* launches,
                         int64_t* outer_iters, int64_t* inner_iters) {
     CHECK_ARG(P, "null handle");
-    if (n_applies) *n_applies = P->n_applies;
-    if (dof_applied) *dof_applied = P->dof_applied;
+    SG_TRY(sync_stats(P));
+    const SolveCtl* c = P->hctl;
+    if (n_applies) *n_applies = P->n_applies + (c ? c->n_applies : 0);
+    if (dof_applied) *dof_applied = P->dof_applied + (c ? (int64_t)c->dof_applied : 0);
     if (launches) *launches = P->launches;
-    if (outer_iters) *outer_iters = P->outer_iters;
-    if (inner_iters) *inner_iters = P->inner_iters;
+    if (outer_iters) *outer_iters = c ? c->outer_iters : 0;
+    if (inner_iters) *inner_iters = c ? c->inner_iters : 0;
+    return SG_OK;
+}
+extern "C" int sg_solver_health(sg_problem* P, int64_t* outer_unconverged, int64_t* outer_nonfinite,
+                                int64_t* inner_maxit, int64_t* inner_breakdowns) {
+    CHECK_ARG(P, "null handle");
+    SG_TRY(sync_stats(P));
+    const SolveCtl* c = P->hctl;
+    if (outer_unconverged) *outer_unconverged = c ? c->outer_unconverged : 0;
+    if (outer_nonfinite) *outer_nonfinite = c ? c->outer_nonfinite : 0;
+    if (inner_maxit) *inner_maxit = c ? c->inner_maxit : 0;
+    if (inner_breakdowns) *inner_breakdowns = c ? c->inner_breakdowns : 0;
     return SG_OK;
 }
 extern "C" int sg_reset_stats(sg_problem* P) {
     CHECK_ARG(P, "null handle");
-    P->n_applies = P->dof_applied = P->launches = P->outer_iters = P->inner_iters = 0;
-    P->mr_switches = 0;
-    SG_CUDA(cudaStreamSynchronize(P->stream));
-    for (auto& pr : P->ev_pairs) {
-        cudaEventDestroy(pr.first);
-        cudaEventDestroy(pr.second);
-    }
-    P->ev_pairs.clear();
-    P->kern_ms = 0;
-    P->kern_launches = 0;
-    P->kern_bytes = P->kern_flops = 0;
-    return SG_OK;
+    P->n_applies = P->dof_applied = P->launches = 0;
+    return reset_device_stats(P);
 }
 extern "C" int sg_set_timing(sg_problem* P, int on) {
     CHECK_ARG(P, "null handle");
@@ -519,24 +484,18 @@ extern "C" int sg_set_timing(sg_problem* P, int on) {
 }
 extern "C" int sg_kernel_time(sg_problem* P, double* ms, int64_t* launches, double* alg_bytes, double* alg_flops) {
     CHECK_ARG(P, "null handle");
-    SG_CUDA(cudaStreamSynchronize(P->stream));
-    for (auto& pr : P->ev_pairs) {
-        float t = 0;
-        SG_CUDA(cudaEventElapsedTime(&t, pr.first, pr.second));
-        P->kern_ms += t;
-        cudaEventDestroy(pr.first);
-        cudaEventDestroy(pr.second);
-    }
-    P->ev_pairs.clear();
-    if (ms) *ms = P->kern_ms;
-    if (launches) *launches = P->kern_launches;
-    if (alg_bytes) *alg_bytes = P->kern_bytes;
-    if (alg_flops) *alg_flops = P->kern_flops;
+    SG_TRY(sync_stats(P));
+    const SolveCtl* c = P->hctl;
+    if (ms) *ms = c ? c->apply_ns * 1e-6 : 0.0;
+    if (launches) *launches = c ? c->timed_applies : 0;
+    if (alg_bytes) *alg_bytes = c ? c->alg_bytes : 0.0;
+    if (alg_flops) *alg_flops = c ? c->alg_flops : 0.0;
     return SG_OK;
 }
 
-extern "C" int sg_outer_switches(const sg_problem* P, int64_t* switches) {
+extern "C" int sg_outer_switches(sg_problem* P, int64_t* switches) {
     CHECK_ARG(P && switches, "null argument");
-    *switches = P->mr_switches;
+    SG_TRY(sync_stats(P));
+    *switches = P->hctl ? P->hctl->mr_switches : 0;
     return SG_OK;
 }

@@ -22,7 +22,8 @@ namespace sg {
 template <int DIR, int W, int NO>
 __global__ void __launch_bounds__(256) k_fanout(int S, int64_t n1, int64_t n2_in, int64_t n1_out, int64_t n2_out,
                                                 const int32_t* __restrict__ cols, const double* __restrict__ in,
-                                                FanoutList fl, int o0) {
+                                                FanoutList fl, int o0, const double* __restrict__ skip) {
+    if (skip && *skip != 0.0) return;   // grid converged (batched block solver)
     const unsigned per_s = (unsigned)(n1_out * n2_out);
     const unsigned total = per_s * (unsigned)S;
     const unsigned n2o = (unsigned)n2_out;
@@ -66,7 +67,8 @@ template <int DIR, int W>
 __global__ void __launch_bounds__(256) k_gather(int S_out, int64_t n1_in, int64_t n2_in, int64_t n1_out,
                                                 int64_t n2_out, const int32_t* __restrict__ cols,
                                                 const __grid_constant__ EntryList el, double* __restrict__ out,
-                                                double beta) {
+                                                double beta, const double* __restrict__ skip) {
+    if (skip && *skip != 0.0) return;   // grid converged (batched block solver)
     const unsigned per_s = (unsigned)(n1_out * n2_out);
     const unsigned total = per_s * (unsigned)S_out;
     const unsigned n2o = (unsigned)n2_out;
@@ -108,7 +110,8 @@ template <int W>
 __global__ void __launch_bounds__(256) k_gather_s2(int64_t n1_in, int64_t n2_in, int64_t n1_out,
                                                    const int32_t* __restrict__ cols,
                                                    const __grid_constant__ EntryList el, double* __restrict__ out,
-                                                   double beta) {
+                                                   double beta, const double* __restrict__ skip) {
+    if (skip && *skip != 0.0) return;   // grid converged (batched block solver)
     const unsigned n2o = (unsigned)n2_in;
     const unsigned per_s = (unsigned)(n1_out * n2_in);
     for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < per_s; t += gridDim.x * blockDim.x) {
@@ -160,13 +163,13 @@ static void fanout_dispatch(sg_problem* P, int S, int64_t n1_in, int64_t n2_in, 
     while (o < fl.no) {
         int left = fl.no - o;
         if (left >= 4) {
-            k_fanout<DIR, W, 4><<<g, 256, 0, P->stream>>>(S, n1_in, n2_in, n1_out, n2_out, cols, in, fl, o);
+            k_fanout<DIR, W, 4><<<g, 256, 0, P->stream>>>(S, n1_in, n2_in, n1_out, n2_out, cols, in, fl, o, P->skip);
             o += 4;
         } else if (left >= 2) {
-            k_fanout<DIR, W, 2><<<g, 256, 0, P->stream>>>(S, n1_in, n2_in, n1_out, n2_out, cols, in, fl, o);
+            k_fanout<DIR, W, 2><<<g, 256, 0, P->stream>>>(S, n1_in, n2_in, n1_out, n2_out, cols, in, fl, o, P->skip);
             o += 2;
         } else {
-            k_fanout<DIR, W, 1><<<g, 256, 0, P->stream>>>(S, n1_in, n2_in, n1_out, n2_out, cols, in, fl, o);
+            k_fanout<DIR, W, 1><<<g, 256, 0, P->stream>>>(S, n1_in, n2_in, n1_out, n2_out, cols, in, fl, o, P->skip);
             o += 1;
         }
         P->launches++;
@@ -206,7 +209,7 @@ int launch_gather(sg_problem* P, int dir, int W, int S_out, int64_t n1_in, int64
             if (el_in.e[e].s_out == s) el.e[el.ne++] = el_in.e[e];
     }
     for (int s = std::min(S_out, 2); s <= 2; ++s) el.sbeg[s] = el.ne;
-    if (dir == 0 && S_out == 2 && P->use_gather_s2 && n1_in * n2_in < (1LL << 31) && nrows_out * n2_in < (1LL << 31)) {
+    if (dir == 0 && S_out == 2 && n1_in * n2_in < (1LL << 31) && nrows_out * n2_in < (1LL << 31)) {
         // sort by (input, s_in) so that entries sharing an input are adjacent
         EntryList es;
         es.ne = el_in.ne;
@@ -216,7 +219,7 @@ int launch_gather(sg_problem* P, int dir, int W, int S_out, int64_t n1_in, int64
         });
         es.sbeg[0] = es.sbeg[1] = es.sbeg[2] = 0;
         const int g = grid_for(nrows_out * n2_in);
-#define GS2(WW) k_gather_s2<WW><<<g, 256, 0, P->stream>>>(n1_in, n2_in, nrows_out, cols, es, out, beta)
+#define GS2(WW) k_gather_s2<WW><<<g, 256, 0, P->stream>>>(n1_in, n2_in, nrows_out, cols, es, out, beta, P->skip)
         if (W == 3) GS2(3); else if (W == 7) GS2(7); else if (W == 15) GS2(15); else if (W == 2) GS2(2);
         else return SG_ERR_ARG;
 #undef GS2
@@ -233,7 +236,7 @@ int launch_gather(sg_problem* P, int dir, int W, int S_out, int64_t n1_in, int64
         return SG_ERR_UNSUPPORTED;
     }
     const int g = grid_for(total);
-#define GA(D, WW) k_gather<D, WW><<<g, 256, 0, P->stream>>>(S_out, n1_in, n2_in, n1_out, n2_out, cols, el, out, beta)
+#define GA(D, WW) k_gather<D, WW><<<g, 256, 0, P->stream>>>(S_out, n1_in, n2_in, n1_out, n2_out, cols, el, out, beta, P->skip)
     if (dir == 1) {
         if (W == 3) GA(1, 3); else if (W == 7) GA(1, 7); else if (W == 15) GA(1, 15); else if (W == 2) GA(1, 2);
         else return SG_ERR_ARG;
@@ -342,7 +345,8 @@ template <int D, int R, int MINB = 2>
 __global__ void __launch_bounds__(VF_TC * VF_RL, MINB) k_vfan_st(int64_t nrows, int64_t n1, int64_t n2, StencilOff so,
                                                               const uint8_t* __restrict__ xflag, VfanParams vp,
                                                               const double* __restrict__ X, int64_t rows_per_block,
-                                                              int64_t opitch) {
+                                                              int64_t opitch, const double* __restrict__ skip) {
+    if (skip && *skip != 0.0) return;   // grid converged (batched block solver)
     constexpr int W = stc::Bands<D>::W;
     extern __shared__ double sm[];
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -394,121 +398,6 @@ __global__ void __launch_bounds__(VF_TC * VF_RL, MINB) k_vfan_st(int64_t nrows, 
     }
 }
 
-// Pass 1, k-outer variant: each thread owns VK rows of one column; for every stencil slot k
-// the VK X values are loaded once and every group's coefficient (one shared-memory load)
-// feeds VK FMAs, halving the coefficient loads per output of k_vfan_st.  Interior groups
-// first (accumulators acc[g][r] for g < ng_int), boundary-only groups in a second sweep
-// on blocks that contain an x-boundary row.
-template <int D, int NGI, int VK>
-__global__ void __launch_bounds__(VF_TC * VF_RL, 2) k_vfan_k(int64_t nrows, int64_t n1, int64_t n2, StencilOff so,
-                                                             const uint8_t* __restrict__ xflag, VfanParams vp,
-                                                             const double* __restrict__ X, int64_t rows_per_block,
-                                                             int64_t opitch) {
-    constexpr int W = stc::Bands<D>::W;
-    extern __shared__ double sm[];
-    __shared__ int soff[16];
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const int a = blockIdx.x * VF_TC + tx;
-    const bool aval = a < n2;
-    const int tot = vp.ng * W * VF_TC;
-    for (int idx = ty * VF_TC + tx; idx < tot; idx += VF_TC * VF_RL) {
-        const int g = idx / (W * VF_TC), rem = idx - g * W * VF_TC, k = rem / VF_TC, c = rem - k * VF_TC;
-        const int ac = blockIdx.x * VF_TC + c;
-        sm[idx] = ac < n2 ? __ldg(vp.vst[g] + (int64_t)k * n2 + ac) : 0.0;
-    }
-    if (ty == 0 && tx < W) soff[tx] = (int)so.off[tx];
-    __syncthreads();
-    const double* xa = X + a;
-    const int64_t rb = blockIdx.y * rows_per_block;
-    const int64_t re = min(nrows, rb + rows_per_block);
-    for (int64_t r0 = rb + ty * VK; r0 < re; r0 += VF_RL * VK) {
-        bool anyb = false;
-#pragma unroll
-        for (int r = 0; r < VK; ++r)
-            if (r0 + r < re) anyb |= xflag[(r0 + r) % n1] != 0;
-        const int nr = (int)min((int64_t)VK, re - r0);
-        const double* xr = xa + r0 * n2;
-        double acc[NGI][VK];
-#pragma unroll
-        for (int g = 0; g < NGI; ++g)
-#pragma unroll
-            for (int r = 0; r < VK; ++r) acc[g][r] = 0.0;
-#pragma unroll 1
-        for (int k = 0; k < W; ++k) {
-            const int o = soff[k];
-            const bool ok = aval && a + o >= 0 && a + o < n2;   // absent neighbours have zero coefficients
-            double xv[VK];
-#pragma unroll
-            for (int r = 0; r < VK; ++r) xv[r] = (ok && r < nr) ? __ldg(xr + r * n2 + o) : 0.0;
-            const double* cp = sm + k * VF_TC + tx;
-#pragma unroll
-            for (int g = 0; g < NGI; ++g) {
-                const double c = cp[g * W * VF_TC];
-#pragma unroll
-                for (int r = 0; r < VK; ++r) acc[g][r] = fma(c, xv[r], acc[g][r]);
-            }
-        }
-        if (aval) {
-#pragma unroll
-            for (int g = 0; g < NGI; ++g) {
-                double* op = vp.out[g] + a;
-#pragma unroll
-                for (int r = 0; r < VK; ++r)
-                    if (r < nr) op[(r0 + r) * opitch] = acc[g][r];
-            }
-        }
-        if (anyb) {
-            for (int g = NGI; g < vp.ng; ++g) {
-                double ab[VK];
-#pragma unroll
-                for (int r = 0; r < VK; ++r) ab[r] = 0.0;
-#pragma unroll 1
-                for (int k = 0; k < W; ++k) {
-                    const int o = soff[k];
-                    const bool ok = aval && a + o >= 0 && a + o < n2;
-                    const double c = sm[(g * W + k) * VF_TC + tx];
-#pragma unroll
-                    for (int r = 0; r < VK; ++r)
-                        ab[r] = fma(c, (ok && r < nr) ? __ldg(xr + r * n2 + o) : 0.0, ab[r]);
-                }
-                if (aval) {
-                    double* op = vp.out[g] + a;
-#pragma unroll
-                    for (int r = 0; r < VK; ++r)
-                        if (r < nr) op[(r0 + r) * opitch] = ab[r];
-                }
-            }
-        }
-    }
-}
-
-int launch_vfan_k(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, const uint8_t* xflag,
-                  const VfanParams& vp, const double* X, int64_t opitch) {
-    if (opitch <= 0) opitch = n2;
-    const int W = (1 << (d + 1)) - 1;
-    const int64_t nrows = (int64_t)S * n1;
-    const int64_t ctiles = (n2 + VF_TC - 1) / VF_TC;
-    int64_t rchunks = std::max<int64_t>(1, (148 * 6 + ctiles - 1) / ctiles);
-    rchunks = std::min<int64_t>(rchunks, (nrows + 31) / 32);
-    rchunks = std::max<int64_t>(rchunks, 1);
-    const int64_t rpb = (nrows + rchunks - 1) / rchunks;
-    const size_t smem = sizeof(double) * vp.ng * W * VF_TC;
-    dim3 grid((unsigned)ctiles, (unsigned)rchunks), block(VF_TC, VF_RL);
-#define VK_L(DD, NG, R)                                                                                      \
-    do {                                                                                                     \
-        cudaFuncSetAttribute(k_vfan_k<DD, NG, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
-        k_vfan_k<DD, NG, R><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch); \
-    } while (0)
-    if (n1 * n2 >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
-    if (d == 3 && vp.ng_int == 10) VK_L(3, 10, 4);
-    else if (d == 2 && vp.ng_int == 6) VK_L(2, 6, 4);
-    else return SG_ERR_UNSUPPORTED;
-#undef VK_L
-    P->launches++;
-    SG_CUDA(cudaGetLastError());
-    return SG_OK;
-}
-
 // Pass 2 (x side): Y[s][i][a] = beta*Y + sum_e [s_out(e)=s] sum_k Cst_e[k][i] Z_e[s_in][i + off_k][a].
 // Block = 8 warps x T consecutive target rows (32 rows); warp lanes = columns,
 // CPT columns per lane.  The block's coefficients (chunk of entries) are staged
@@ -518,7 +407,8 @@ constexpr int XG_ECH = 12;   // entries per shared-memory chunk
 template <int D, int T, int SO, int CPT>
 __global__ void __launch_bounds__(256, 2) k_xgat_st(int n1, int n2, StencilOff so, const uint8_t* __restrict__ xflag,
                                                     XgatParams ep, double* __restrict__ Y, double beta,
-                                                    int ncoltiles, int m) {
+                                                    int ncoltiles, int m, const double* __restrict__ skip) {
+    if (skip && *skip != 0.0) return;   // grid converged (batched block solver)
     using B = stc::Bands<D>;
     constexpr int W = B::W;
     constexpr int ROWS = 8 * T;
@@ -920,7 +810,7 @@ int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const St
     const int64_t nrows = (int64_t)S * n1;
     const int64_t ctiles = (n2 + VF_TC - 1) / VF_TC;
     // enough blocks to fill the machine, as many rows per block as possible (coefficient reuse)
-    static const int vf_mult = getenv("SG_VF_BLK") ? atoi(getenv("SG_VF_BLK")) : 12;   // 12 per SM measured best
+    constexpr int vf_mult = 12;   // blocks per SM, measured best in round 1
     int64_t rchunks = std::max<int64_t>(1, (148 * vf_mult + ctiles - 1) / ctiles);
     rchunks = std::min<int64_t>(rchunks, (nrows + 15) / 16);
     rchunks = std::max<int64_t>(rchunks, 1);
@@ -929,24 +819,14 @@ int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const St
     dim3 grid((unsigned)ctiles, (unsigned)rchunks), block(VF_TC, VF_RL);
     if (d == 1) {
         cudaFuncSetAttribute(k_vfan_st<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_vfan_st<1, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch);
+        k_vfan_st<1, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch, P->skip);
     } else if (d == 2) {
         cudaFuncSetAttribute(k_vfan_st<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_vfan_st<2, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch);
+        k_vfan_st<2, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch, P->skip);
     } else {
-        // rows per thread on 3D v-lattices (SG_VF_R = 3/4: more coefficient reuse per shared load,
-        // one resident block of registers per thread pair)
-        const int vf_r = getenv("SG_VF_R") ? atoi(getenv("SG_VF_R")) : 2;
-        if (vf_r == 4) {
-            cudaFuncSetAttribute(k_vfan_st<3, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_vfan_st<3, 4, 1><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch);
-        } else if (vf_r == 3) {
-            cudaFuncSetAttribute(k_vfan_st<3, 3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_vfan_st<3, 3, 1><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch);
-        } else {
-            cudaFuncSetAttribute(k_vfan_st<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_vfan_st<3, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch);
-        }
+        // R = 2 rows per thread (R = 3/4 measured 4-11 % slower in round 1: register-starved)
+        cudaFuncSetAttribute(k_vfan_st<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_vfan_st<3, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch, P->skip);
     }
     P->launches++;
     SG_CUDA(cudaGetLastError());
@@ -956,8 +836,7 @@ int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const St
 int launch_xgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
                    const uint8_t* xflag, const XgatParams& ep, double* Y, double beta, int m) {
     constexpr int T = 4;
-    static const int cpt_env = getenv("SG_XG_CPT") ? atoi(getenv("SG_XG_CPT")) : 0;
-    const int cpt = cpt_env == 1 ? 1 : (n2 >= 64 ? 2 : 1);
+    const int cpt = n2 >= 64 ? 2 : 1;
     const int64_t ctiles = (n2 + 32 * cpt - 1) / (32 * cpt);
     const int64_t rgroups = (n1 + 8 * T - 1) / (8 * T);
     const int64_t nb = ctiles * rgroups;
@@ -965,7 +844,7 @@ int launch_xgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, cons
         set_error("grid too large for 32-bit stencil indexing");
         return SG_ERR_UNSUPPORTED;
     }
-#define XG(DD, SS, CC) k_xgat_st<DD, T, SS, CC><<<(unsigned)nb, 256, 0, P->stream>>>((int)n1, (int)n2, so, xflag, ep, Y, beta, (int)ctiles, m)
+#define XG(DD, SS, CC) k_xgat_st<DD, T, SS, CC><<<(unsigned)nb, 256, 0, P->stream>>>((int)n1, (int)n2, so, xflag, ep, Y, beta, (int)ctiles, m, P->skip)
 #define XGD(SS, CC) do { if (d == 1) XG(1, SS, CC); else if (d == 2) XG(2, SS, CC); else XG(3, SS, CC); } while (0)
     if (S_out == 1) {
         if (cpt == 2) XGD(1, 2); else XGD(1, 1);
@@ -979,140 +858,6 @@ int launch_xgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, cons
     return SG_OK;
 }
 
-}  // namespace sg
-
-namespace sg {
-// =====================================================================
-// Fused single-pass strip operator for grids whose x factor is small
-// ("whole-x", v-first): one block owns 32 v-columns and ALL S*n1 rows, so the
-// intermediates Z_b = (Id x Id x B_b) X never leave shared memory and X is
-// read once / Y written once (PAPER.md l.516-532 ordering, S^(2) first).
-//   smem: Ysm[S*n1][32] accumulator + Zsm[GC][S*n1][32] for a chunk of GC groups
-// =====================================================================
-constexpr int FW_WARPS = 16;
-template <int DV, int DX>
-__global__ void __launch_bounds__(FW_WARPS * 32, 1) k_fused_wx(int S, int n1, int n2, StencilOff sov, StencilOff sox,
-                                                               int mx, const uint8_t* __restrict__ xflag, VfanParams vp,
-                                                               XgatParams ep, const int* __restrict__ egrp, int GC,
-                                                               const double* __restrict__ X, double* __restrict__ Y) {
-    constexpr int WV = stc::Bands<DV>::W;
-    constexpr int WX = stc::Bands<DX>::W;
-    extern __shared__ double smf[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int R = S * n1;
-    double* Bsm = smf;                                  // [ng][WV][32]
-    double* Ysm = Bsm + (size_t)vp.ng * WV * 32;         // [R][32]
-    double* Zsm = Ysm + (size_t)R * 32;                  // [GC][R][32]
-    const int a = blockIdx.x * 32 + lane;
-    const bool aval = a < n2;
-    for (int idx = threadIdx.x; idx < vp.ng * WV * 32; idx += FW_WARPS * 32) {
-        const int g = idx / (WV * 32), rem = idx - g * WV * 32, k = rem >> 5, c = rem & 31;
-        const int ac = blockIdx.x * 32 + c;
-        Bsm[idx] = ac < n2 ? __ldg(vp.vst[g] + (long long)k * n2 + ac) : 0.0;
-    }
-    int addr[WV];
-#pragma unroll
-    for (int k = 0; k < WV; ++k) {
-        int c = a + (int)sov.off[k];
-        addr[k] = c < 0 ? 0 : (c >= n2 ? n2 - 1 : c);
-    }
-    for (int r = warp; r < R; r += FW_WARPS) Ysm[r * 32 + lane] = 0.0;
-    for (int g0 = 0; g0 < vp.ng; g0 += GC) {
-        const int gc = min(GC, vp.ng - g0);
-        __syncthreads();
-        // stage A: Z_g = B_g X along v for the chunk's groups; X row loaded once per chunk
-        for (int r = warp; r < R; r += FW_WARPS) {
-            const double* xr = X + (long long)r * n2;
-            double x[WV];
-#pragma unroll
-            for (int k = 0; k < WV; ++k) x[k] = aval ? __ldg(xr + addr[k]) : 0.0;
-            const bool bnd = xflag[r % n1] != 0;
-            for (int gi = 0; gi < gc; ++gi) {
-                const int g = g0 + gi;
-                double z = 0.0;
-                if (bnd || g < vp.ng_int) {
-                    const double* Bg = Bsm + (size_t)g * WV * 32 + lane;
-#pragma unroll
-                    for (int k = 0; k < WV; ++k) z = fma(Bg[k * 32], x[k], z);
-                }
-                Zsm[((size_t)gi * R + r) * 32 + lane] = z;
-            }
-        }
-        __syncthreads();
-        // stage B: x-stencil of the chunk's Z into the accumulator
-        for (int r = warp; r < R; r += FW_WARPS) {
-            const int s = r / n1, i = r - s * n1;
-            const bool bnd = xflag[i] != 0;
-            int cls = 0;
-            {
-                int z = i, mul = 1;
-#pragma unroll
-                for (int q = 0; q < DX; ++q) {
-                    const int zq = z % mx;
-                    z /= mx;
-                    cls += mul * (zq == 0 ? 0 : (zq == mx - 1 ? 2 : 1));
-                    mul *= 3;
-                }
-            }
-            int src[WX];
-#pragma unroll
-            for (int k = 0; k < WX; ++k) {
-                int q = i + (int)sox.off[k];
-                src[k] = q < 0 ? 0 : (q >= n1 ? n1 - 1 : q);
-            }
-            double acc = Ysm[r * 32 + lane];
-            for (int e = 0; e < ep.ne; ++e) {
-                const int ge = egrp[e];
-                if (ge < g0 || ge >= g0 + gc) continue;
-                const XgatEntry& E = ep.e[e];
-                if (E.s_out != s || (E.bonly && !bnd)) continue;
-                const double* Zg = Zsm + ((size_t)(ge - g0) * R + (size_t)E.s_in * n1) * 32 + lane;
-                double t = 0.0;
-#pragma unroll
-                for (int k = 0; k < WX; ++k) {
-                    const double cf = E.ctab ? __ldg(E.ctab + cls * WX + k) : __ldg(E.cst + (long long)k * n1 + i);
-                    t = fma(cf, Zg[src[k] * 32], t);
-                }
-                acc = fma(E.scale, t, acc);
-            }
-            Ysm[r * 32 + lane] = acc;
-        }
-    }
-    __syncthreads();
-    if (!aval) return;
-    for (int r = warp; r < R; r += FW_WARPS) Y[(long long)r * n2 + a] = Ysm[r * 32 + lane];
-}
-
-// returns SG_ERR_UNSUPPORTED if the tile does not fit (caller uses the 2-pass path)
-int launch_fused_wx(sg_problem* P, int dv, int dx, int S, int64_t n1, int64_t n2, const StencilOff& sov,
-                    const StencilOff& sox, int mx, const uint8_t* xflag, const VfanParams& vp, const XgatParams& ep,
-                    const int* egrp_dev, const double* X, double* Y) {
-    const size_t row_bytes = (size_t)S * n1 * 32 * sizeof(double);
-    const int WV = (1 << (dv + 1)) - 1;
-    const size_t coef_bytes = (size_t)vp.ng * WV * 32 * sizeof(double);
-    const size_t budget = 220 * 1024;
-    if (coef_bytes + 2 * row_bytes > budget || n1 * n2 >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
-    int GC = (int)((budget - coef_bytes) / row_bytes) - 1;
-    GC = std::max(1, std::min(GC, vp.ng));
-    // many chunks re-read X from L2 each time: prefer the two-pass path then
-    if ((vp.ng + GC - 1) / GC > 4) return SG_ERR_UNSUPPORTED;
-    const size_t smem = coef_bytes + row_bytes * (1 + GC);
-    const unsigned nb = (unsigned)((n2 + 31) / 32);
-#define FW(A, B)                                                                                          \
-    do {                                                                                                  \
-        cudaFuncSetAttribute(k_fused_wx<A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
-        k_fused_wx<A, B><<<nb, FW_WARPS * 32, smem, P->stream>>>(S, (int)n1, (int)n2, sov, sox, mx, xflag, vp, ep, \
-                                                       egrp_dev, GC, X, Y);                               \
-    } while (0)
-    if (dv == 1 && dx == 1) FW(1, 1);
-    else if (dv == 2 && dx == 2) FW(2, 2);
-    else if (dv == 3 && dx == 3) FW(3, 3);
-    else return SG_ERR_UNSUPPORTED;
-#undef FW
-    P->launches++;
-    SG_CUDA(cudaGetLastError());
-    return SG_OK;
-}
 }  // namespace sg
 
 namespace sg {
@@ -1159,75 +904,6 @@ __global__ void __launch_bounds__(256) k_jobs(JobList jl) {
             J.out[((size_t)s * n1_out + r) * (size_t)J.opitch + c] = v;
         else
             J.out[t] = v;
-    }
-}
-
-// Warp-unit variant: a warp owns one unit of a job —
-//   dir 0 (transfer along the x rows): one output row r and a chunk of JB_CH columns; the
-//         row's W (col, val) pairs are loaded once and every lane streams columns;
-//   dir 1 (transfer along the v columns): 32 output columns (lane = column) and JB_RC rows;
-//         each lane loads its column's W pairs once and streams the rows.
-// No per-element index division; coefficient/pattern loads amortised over the unit.
-constexpr int JB_CH = 1024, JB_RC = 16;
-__device__ __forceinline__ int64_t job_units(const Job& J) {
-    if (J.dir == 0) return (int64_t)J.S * J.nrows_out * ((J.n2_in + JB_CH - 1) / JB_CH);
-    return ((J.nrows_out + 31) / 32) * (((int64_t)J.S * J.n1_in + JB_RC - 1) / JB_RC);
-}
-__global__ void __launch_bounds__(256) k_jobs2(JobList jl) {
-    int j = 0;
-    while (j + 1 < jl.nj && jl.j[j + 1].blk0 <= (int)blockIdx.x) ++j;
-    const Job& J = jl.j[j];
-    const int lane = threadIdx.x & 31;
-    const int64_t u = (int64_t)(blockIdx.x - J.blk0) * 8 + (threadIdx.x >> 5);
-    if (u >= job_units(J)) return;
-    const int W = J.W;
-    if (J.dir == 0) {
-        const int64_t n2 = J.n2_in, nch = (n2 + JB_CH - 1) / JB_CH;
-        const int64_t rowidx = u / nch, ch = u - rowidx * nch;
-        const int64_t s = rowidx / J.nrows_out, r = rowidx - s * J.nrows_out;
-        int32_t col[15];
-        double val[15];
-#pragma unroll
-        for (int k = 0; k < 15; ++k) {
-            col[k] = k < W ? __ldg(J.cols + k * J.nrows_out + r) : -1;
-            val[k] = k < W && col[k] >= 0 ? __ldg(J.vals + k * J.nrows_out + r) : 0.0;
-        }
-        const double* in = J.in + (size_t)s * J.n1_in * n2;
-        const int64_t obase = (s * J.nrows_out + r) * (J.opitch > 0 ? J.opitch : n2);
-        const int64_t abase = (s * J.nrows_out + r) * n2;
-        const int64_t c1 = min(n2, (ch + 1) * JB_CH);
-#pragma unroll 4
-        for (int64_t c = ch * JB_CH + lane; c < c1; c += 32) {
-            double acc = 0.0;
-#pragma unroll
-            for (int k = 0; k < 15; ++k)
-                if (k < W && col[k] >= 0) acc = fma(val[k], __ldg(in + (size_t)col[k] * n2 + c), acc);
-            J.out[obase + c] = (J.add ? J.add[abase + c] : 0.0) + J.scale * acc;
-        }
-    } else {
-        const int64_t nct = (J.nrows_out + 31) / 32;
-        const int64_t rc = u / nct, ct = u - rc * nct;
-        const int64_t c = ct * 32 + lane;
-        if (c >= J.nrows_out) return;
-        int32_t col[15];
-        double val[15];
-#pragma unroll
-        for (int k = 0; k < 15; ++k) {
-            col[k] = k < W ? __ldg(J.cols + k * J.nrows_out + c) : -1;
-            val[k] = k < W && col[k] >= 0 ? __ldg(J.vals + k * J.nrows_out + c) : 0.0;
-        }
-        const int64_t nrows = (int64_t)J.S * J.n1_in;
-        const int64_t r1 = min(nrows, (rc + 1) * JB_RC);
-        const int64_t op = J.opitch > 0 ? J.opitch : J.nrows_out;
-#pragma unroll 4
-        for (int64_t rr = rc * JB_RC; rr < r1; ++rr) {
-            const double* in = J.in + rr * J.n2_in;
-            double acc = 0.0;
-#pragma unroll
-            for (int k = 0; k < 15; ++k)
-                if (k < W && col[k] >= 0) acc = fma(val[k], __ldg(in + col[k]), acc);
-            J.out[rr * op + c] = (J.add ? J.add[rr * J.nrows_out + c] : 0.0) + J.scale * acc;
-        }
     }
 }
 
@@ -1340,35 +1016,6 @@ __global__ void __launch_bounds__(256) k_jobs_pbox(JobList jl) {
 }
 
 int launch_jobs(sg_problem* P, std::vector<Job>& jobs) {
-    if (P->use_jobs2) {
-        size_t i = 0;
-        while (i < jobs.size()) {
-            JobList jl;
-            jl.nj = 0;
-            int blk = 0;
-            while (i < jobs.size() && jl.nj < MAX_JOBS) {
-                Job J = jobs[i++];
-                if (J.W > 15) {
-                    set_error("transfer job wider than 15");
-                    return SG_ERR_UNSUPPORTED;
-                }
-                int64_t units = J.dir == 0 ? (int64_t)J.S * J.nrows_out * ((J.n2_in + JB_CH - 1) / JB_CH)
-                                           : ((J.nrows_out + 31) / 32) * (((int64_t)J.S * J.n1_in + JB_RC - 1) / JB_RC);
-                if (units == 0) continue;
-                const int64_t nb = (units + 7) / 8;
-                if (nb + blk >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
-                J.blk0 = blk;
-                blk += (int)nb;
-                jl.j[jl.nj++] = J;
-            }
-            if (jl.nj == 0) continue;
-            jl.total_blocks = blk;
-            k_jobs2<<<blk, 256, 0, P->stream>>>(jl);
-            P->launches++;
-            SG_CUDA(cudaGetLastError());
-        }
-        return SG_OK;
-    }
     size_t i = 0;
     while (i < jobs.size()) {
         JobList jl;
@@ -1390,10 +1037,10 @@ int launch_jobs(sg_problem* P, std::vector<Job>& jobs) {
         }
         if (jl.nj == 0) continue;
         jl.total_blocks = blk;
-        bool rbox = P->use_rbox;
+        bool rbox = true;
         for (int q = 0; q < jl.nj; ++q) rbox &= jl.j[q].box_mf > 0 && jl.j[q].W == jl.j[0].W;
         const int dd = jl.j[0].W == 3 ? 1 : (jl.j[0].W == 7 ? 2 : (jl.j[0].W == 15 ? 3 : 0));
-        bool pbox = P->use_rbox;
+        bool pbox = true;
         for (int q = 0; q < jl.nj; ++q) pbox &= jl.j[q].box_mf > 0 && jl.j[q].W == 2 && jl.j[q].box_d == jl.j[0].box_d;
         if (pbox && jl.j[0].box_d == 3) k_jobs_pbox<3><<<blk, 256, 0, P->stream>>>(jl);
         else if (pbox && jl.j[0].box_d == 2) k_jobs_pbox<2><<<blk, 256, 0, P->stream>>>(jl);
@@ -1405,429 +1052,6 @@ int launch_jobs(sg_problem* P, std::vector<Job>& jobs) {
         P->launches++;
         SG_CUDA(cudaGetLastError());
     }
-    return SG_OK;
-}
-}  // namespace sg
-
-namespace sg {
-// =====================================================================
-// x-side gather (pass 2) for 3D box x-lattices with 2x2x2 register bricks.
-// Warp = one brick of 8 target rows (lattice z0 + {0,1}^3) x 32*CPT columns.
-// Every source row of the brick's halo is loaded once and scattered into all
-// targets whose Kuhn stencil contains it (static, fully unrolled); interior
-// bricks of translation-invariant matrices use 15 warp-uniform coefficients.
-// Slot k <-> lattice offset (sorted lexicographic linear offsets, m >= 3):
-// =====================================================================
-__host__ __device__ constexpr int kuhn3_slot(int dx, int dy, int dz) {
-    // returns slot 0..14 or -1 if (dx,dy,dz) is not a Kuhn offset
-    return (dx == -1 && dy == -1 && dz == -1) ? 0 :
-           (dx == 0 && dy == -1 && dz == -1) ? 1 :
-           (dx == -1 && dy == 0 && dz == -1) ? 2 :
-           (dx == 0 && dy == 0 && dz == -1) ? 3 :
-           (dx == -1 && dy == -1 && dz == 0) ? 4 :
-           (dx == 0 && dy == -1 && dz == 0) ? 5 :
-           (dx == -1 && dy == 0 && dz == 0) ? 6 :
-           (dx == 0 && dy == 0 && dz == 0) ? 7 :
-           (dx == 1 && dy == 0 && dz == 0) ? 8 :
-           (dx == 0 && dy == 1 && dz == 0) ? 9 :
-           (dx == 1 && dy == 1 && dz == 0) ? 10 :
-           (dx == 0 && dy == 0 && dz == 1) ? 11 :
-           (dx == 1 && dy == 0 && dz == 1) ? 12 :
-           (dx == 0 && dy == 1 && dz == 1) ? 13 :
-           (dx == 1 && dy == 1 && dz == 1) ? 14 : -1;
-}
-
-template <int SO, int CPT>
-__global__ void __launch_bounds__(256, 1) k_xgat_brick3(int n1, int n2, int m, const uint8_t* __restrict__ xflag,
-                                                        XgatParams ep, double* __restrict__ Y, double beta,
-                                                        int ncoltiles) {
-    constexpr int W = 15;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nbx = (m + 1) / 2;
-    const long long nbricks = (long long)nbx * nbx * nbx;
-    const long long bid = (long long)(blockIdx.x / ncoltiles) * 8 + warp;
-    const int ct = blockIdx.x % ncoltiles;
-    if (bid >= nbricks) return;
-    const int bx = (int)(bid % nbx), by = (int)((bid / nbx) % nbx), bz = (int)(bid / ((long long)nbx * nbx));
-    const int x0 = 2 * bx, y0 = 2 * by, z0 = 2 * bz;
-    int acol[CPT];
-    bool aval[CPT];
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-        acol[c] = ct * 32 * CPT + c * 32 + lane;
-        aval[c] = acol[c] < n2;
-        if (!aval[c]) acol[c] = 0;
-    }
-    // target validity and interior test (class 13 = interior in every axis: 1 + 3 + 9)
-    bool tval[8];
-    bool anyb = false, allint = true;
-    int tcls[8];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-        const int x = x0 + (t & 1), y = y0 + ((t >> 1) & 1), z = z0 + (t >> 2);
-        tval[t] = x < m && y < m && z < m;
-        const int cx = x == 0 ? 0 : (x == m - 1 ? 2 : 1), cy = y == 0 ? 0 : (y == m - 1 ? 2 : 1),
-                  cz = z == 0 ? 0 : (z == m - 1 ? 2 : 1);
-        tcls[t] = cx + 3 * cy + 9 * cz;
-        if (tval[t]) {
-            const bool b = xflag[x + (long long)m * (y + (long long)m * z)] != 0;
-            anyb |= b;
-            allint &= (tcls[t] == 13);
-        }
-    }
-    // source rows of the 4x4x4 halo (clamped into the lattice)
-    auto srow = [&](int qx, int qy, int qz) -> long long {
-        int x = x0 + qx, y = y0 + qy, z = z0 + qz;
-        x = x < 0 ? 0 : (x >= m ? m - 1 : x);
-        y = y < 0 ? 0 : (y >= m ? m - 1 : y);
-        z = z < 0 ? 0 : (z >= m ? m - 1 : z);
-        return x + (long long)m * (y + (long long)m * z);
-    };
-    const long long plane = (long long)n1 * n2;
-    double acc[SO][8][CPT];
-#pragma unroll
-    for (int s = 0; s < SO; ++s)
-#pragma unroll
-        for (int t = 0; t < 8; ++t)
-#pragma unroll
-            for (int c = 0; c < CPT; ++c) acc[s][t][c] = 0.0;
-    for (int e = 0; e < ep.ne; ++e) {
-        const XgatEntry& E = ep.e[e];
-        if (E.bonly && !anyb) continue;
-        const double* Z = E.in + (long long)E.s_in * plane;
-        double tmp[8][CPT];
-#pragma unroll
-        for (int t = 0; t < 8; ++t)
-#pragma unroll
-            for (int c = 0; c < CPT; ++c) tmp[t][c] = 0.0;
-        if (allint && E.ctab) {
-            double cf[W];
-#pragma unroll
-            for (int k = 0; k < W; ++k) cf[k] = __ldg(E.ctab + 13 * W + k);
-#pragma unroll
-            for (int qz = -1; qz <= 2; ++qz)
-#pragma unroll
-                for (int qy = -1; qy <= 2; ++qy)
-#pragma unroll
-                    for (int qx = -1; qx <= 2; ++qx) {
-                        bool used = false;
-#pragma unroll
-                        for (int t = 0; t < 8; ++t)
-                            used |= kuhn3_slot(qx - (t & 1), qy - ((t >> 1) & 1), qz - (t >> 2)) >= 0;
-                        if (!used) continue;
-                        const double* zr = Z + srow(qx, qy, qz) * n2;
-                        double zv[CPT];
-#pragma unroll
-                        for (int c = 0; c < CPT; ++c) zv[c] = __ldg(zr + acol[c]);
-#pragma unroll
-                        for (int t = 0; t < 8; ++t) {
-                            const int k = kuhn3_slot(qx - (t & 1), qy - ((t >> 1) & 1), qz - (t >> 2));
-                            if (k >= 0)
-#pragma unroll
-                                for (int c = 0; c < CPT; ++c) tmp[t][c] = fma(cf[k], zv[c], tmp[t][c]);
-                        }
-                    }
-        } else {
-#pragma unroll
-            for (int qz = -1; qz <= 2; ++qz)
-#pragma unroll
-                for (int qy = -1; qy <= 2; ++qy)
-#pragma unroll
-                    for (int qx = -1; qx <= 2; ++qx) {
-                        bool used = false;
-#pragma unroll
-                        for (int t = 0; t < 8; ++t)
-                            used |= kuhn3_slot(qx - (t & 1), qy - ((t >> 1) & 1), qz - (t >> 2)) >= 0;
-                        if (!used) continue;
-                        const double* zr = Z + srow(qx, qy, qz) * n2;
-                        double zv[CPT];
-#pragma unroll
-                        for (int c = 0; c < CPT; ++c) zv[c] = __ldg(zr + acol[c]);
-#pragma unroll
-                        for (int t = 0; t < 8; ++t) {
-                            const int k = kuhn3_slot(qx - (t & 1), qy - ((t >> 1) & 1), qz - (t >> 2));
-                            if (k >= 0 && tval[t]) {
-                                const int x = x0 + (t & 1), y = y0 + ((t >> 1) & 1), z = z0 + (t >> 2);
-                                const long long it = x + (long long)m * (y + (long long)m * z);
-                                const double cfk = E.ctab ? __ldg(E.ctab + tcls[t] * W + k) : __ldg(E.cst + (long long)k * n1 + it);
-#pragma unroll
-                                for (int c = 0; c < CPT; ++c) tmp[t][c] = fma(cfk, zv[c], tmp[t][c]);
-                            }
-                        }
-                    }
-        }
-#pragma unroll
-        for (int s = 0; s < SO; ++s)
-            if (s == E.s_out)
-#pragma unroll
-                for (int t = 0; t < 8; ++t)
-#pragma unroll
-                    for (int c = 0; c < CPT; ++c) acc[s][t][c] = fma(E.scale, tmp[t][c], acc[s][t][c]);
-    }
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-        if (!tval[t]) continue;
-        const int x = x0 + (t & 1), y = y0 + ((t >> 1) & 1), z = z0 + (t >> 2);
-        const long long it = x + (long long)m * (y + (long long)m * z);
-#pragma unroll
-        for (int s = 0; s < SO; ++s) {
-            double* yr = Y + s * plane + it * n2;
-#pragma unroll
-            for (int c = 0; c < CPT; ++c) {
-                if (!aval[c]) continue;
-                double* y = yr + acol[c];
-                *y = beta == 0.0 ? acc[s][t][c] : fma(beta, *y, acc[s][t][c]);
-            }
-        }
-    }
-}
-
-int launch_xgat_brick3(sg_problem* P, int S_out, int64_t n1, int64_t n2, int m, const uint8_t* xflag,
-                       const XgatParams& ep, double* Y, double beta) {
-    const int cpt = n2 >= 64 ? 2 : 1;
-    const int64_t ctiles = (n2 + 32 * cpt - 1) / (32 * cpt);
-    const int64_t nbx = (m + 1) / 2;
-    const int64_t nbricks = nbx * nbx * nbx;
-    const int64_t nb = ctiles * ((nbricks + 7) / 8);
-    if (n1 * n2 >= (1LL << 31) || nb >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
-#define XB(SS, CC) k_xgat_brick3<SS, CC><<<(unsigned)nb, 256, 0, P->stream>>>((int)n1, (int)n2, m, xflag, ep, Y, beta, (int)ctiles)
-    if (S_out == 1) {
-        if (cpt == 2) XB(1, 2); else XB(1, 1);
-    } else {
-        if (cpt == 2) XB(2, 2); else XB(2, 1);
-    }
-#undef XB
-    P->launches++;
-    SG_CUDA(cudaGetLastError());
-    return SG_OK;
-}
-}  // namespace sg
-
-namespace sg {
-// =====================================================================
-// Register-coefficient variants (round-1 "reg" kernels).
-// Each multiply-add needs a coefficient and a value; keeping the coefficient in
-// registers and reusing every loaded value for several FMAs is what lifts the
-// FMA/load ratio above 1 on sm_100a (see profiles/README.md sec. 4).
-// =====================================================================
-
-// Pass 1: Z_g[row][a] = sum_k B_g[k][a] X[row][a + off_k].  Thread = (column a,
-// set of VR_G groups); its coefficients stay in registers while it sweeps the
-// rows of its block; the X values of a row are shared by the VR_G groups.
-constexpr int VR_G = 4;
-template <int D>
-__global__ void __launch_bounds__(256, 2) k_vfan_reg(int nrows, int n1, int n2, StencilOff so,
-                                                     const uint8_t* __restrict__ xflag, VfanParams vp,
-                                                     const double* __restrict__ X, int rows_per_block, int nsets) {
-    constexpr int W = stc::Bands<D>::W;
-    const int cols_per_block = 256 / nsets;
-    const int tid = threadIdx.x;
-    const int cl = tid / nsets, set = tid - cl * nsets;
-    if (cl >= cols_per_block) return;
-    const int a = blockIdx.x * cols_per_block + cl;
-    if (a >= n2) return;
-    const int g0 = set * VR_G;
-    double B[VR_G][W];
-    bool gon[VR_G], gbonly[VR_G];
-#pragma unroll
-    for (int q = 0; q < VR_G; ++q) {
-        const int g = g0 + q;
-        gon[q] = g < vp.ng;
-        gbonly[q] = g >= vp.ng_int;
-#pragma unroll
-        for (int k = 0; k < W; ++k) B[q][k] = gon[q] ? __ldg(vp.vst[g] + (long long)k * n2 + a) : 0.0;
-    }
-    int addr[W];
-#pragma unroll
-    for (int k = 0; k < W; ++k) {
-        int c = a + (int)so.off[k];
-        addr[k] = c < 0 ? 0 : (c >= n2 ? n2 - 1 : c);
-    }
-    const int rb = blockIdx.y * rows_per_block;
-    const int re = min(nrows, rb + rows_per_block);
-    for (int r = rb; r < re; ++r) {
-        const bool bnd = xflag[r % n1] != 0;
-        bool any = false;
-#pragma unroll
-        for (int q = 0; q < VR_G; ++q) any |= gon[q] && (bnd || !gbonly[q]);
-        if (!any) continue;
-        const double* xr = X + (long long)r * n2;
-        double x[W];
-#pragma unroll
-        for (int k = 0; k < W; ++k) x[k] = __ldg(xr + addr[k]);
-#pragma unroll
-        for (int q = 0; q < VR_G; ++q) {
-            if (!gon[q] || (gbonly[q] && !bnd)) continue;
-            double acc = 0.0;
-#pragma unroll
-            for (int k = 0; k < W; ++k) acc = fma(B[q][k], x[k], acc);
-            vp.out[g0 + q][(long long)r * n2 + a] = acc;
-        }
-    }
-}
-
-int launch_vfan_reg(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, const uint8_t* xflag,
-                    const VfanParams& vp, const double* X) {
-    const int nsets = (vp.ng + VR_G - 1) / VR_G;
-    if (nsets > 8 || (int64_t)S * n1 * n2 >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
-    const int cpb = 256 / nsets;
-    const int64_t nrows = (int64_t)S * n1;
-    const int64_t ctiles = (n2 + cpb - 1) / cpb;
-    int64_t rchunks = std::max<int64_t>(1, (148 * 4 + ctiles - 1) / ctiles);
-    rchunks = std::min<int64_t>(rchunks, std::max<int64_t>(1, nrows / 8));
-    rchunks = std::min<int64_t>(rchunks, 65535);
-    const int rpb = (int)((nrows + rchunks - 1) / rchunks);
-    dim3 grid((unsigned)ctiles, (unsigned)rchunks);
-    if (d == 1) k_vfan_reg<1><<<grid, 256, 0, P->stream>>>((int)nrows, (int)n1, (int)n2, so, xflag, vp, X, rpb, nsets);
-    else if (d == 2) k_vfan_reg<2><<<grid, 256, 0, P->stream>>>((int)nrows, (int)n1, (int)n2, so, xflag, vp, X, rpb, nsets);
-    else k_vfan_reg<3><<<grid, 256, 0, P->stream>>>((int)nrows, (int)n1, (int)n2, so, xflag, vp, X, rpb, nsets);
-    P->launches++;
-    SG_CUDA(cudaGetLastError());
-    return SG_OK;
-}
-
-// Pass 2: Y[s][i][a] = sum_e sum_k C_e[i,k] Z_e[s_in][i + off_k][a].  Block = 8 warps
-// sharing XR_T consecutive target rows x 32 columns; warp w owns the entries
-// e = w, w+8, ...; interior targets of translation-invariant matrices use
-// register coefficients; partial sums are reduced through shared memory.
-constexpr int XR_T = 8;
-template <int D, int SO>
-__global__ void __launch_bounds__(256, 2) k_xgat_reg(int n1, int n2, StencilOff so, int m,
-                                                     const uint8_t* __restrict__ xflag, XgatParams ep,
-                                                     double* __restrict__ Y, double beta, int ncoltiles) {
-    using B = stc::Bands<D>;
-    constexpr int W = B::W;
-    constexpr int MAXL = 3;
-    __shared__ double red[8][SO][XR_T][32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int rgroups = (n1 + XR_T - 1) / XR_T;
-    const int ct = blockIdx.x / rgroups, rg = blockIdx.x % rgroups;
-    const int i0 = rg * XR_T;
-    const int a = ct * 32 + lane;
-    const bool aval = a < n2;
-    const int ac = aval ? a : 0;
-    int cls[XR_T];
-    bool anyb = false, allint = true;
-#pragma unroll
-    for (int t = 0; t < XR_T; ++t) {
-        const int it = min(i0 + t, n1 - 1);
-        int z = it, c = 0, mul = 1, interior = 1;
-#pragma unroll
-        for (int q = 0; q < D; ++q) {
-            const int zq = z % m;
-            z /= m;
-            const int st = zq == 0 ? 0 : (zq == m - 1 ? 2 : 1);
-            interior &= st == 1;
-            c += mul * st;
-            mul *= 3;
-        }
-        cls[t] = c;
-        if (i0 + t < n1) {
-            anyb |= xflag[it] != 0;
-            allint &= interior != 0;
-        }
-    }
-    int icls = 0;
-    {
-        int mul = 1;
-#pragma unroll
-        for (int q = 0; q < D; ++q) {
-            icls += mul;
-            mul *= 3;
-        }
-    }
-    const long long plane = (long long)n1 * n2;
-    double acc[SO][XR_T];
-#pragma unroll
-    for (int s = 0; s < SO; ++s)
-#pragma unroll
-        for (int t = 0; t < XR_T; ++t) acc[s][t] = 0.0;
-    for (int e = warp; e < ep.ne; e += 8) {
-        const XgatEntry& E = ep.e[e];
-        if (E.bonly && !anyb) continue;
-        const double* Z = E.in + (long long)E.s_in * plane;
-        const bool fast = allint && E.ctab != nullptr;
-        double cf[W];
-        if (fast) {
-#pragma unroll
-            for (int k = 0; k < W; ++k) cf[k] = __ldg(E.ctab + icls * W + k);
-        }
-        double tmp[XR_T];
-#pragma unroll
-        for (int t = 0; t < XR_T; ++t) tmp[t] = 0.0;
-#pragma unroll
-        for (int b = 0; b < B::NB; ++b) {
-            const int klo = B::lo(b), len = B::len(b);
-            const int base = i0 + (int)so.off[klo];
-            double z[XR_T + MAXL - 1];
-#pragma unroll
-            for (int q = 0; q < XR_T + MAXL - 1; ++q) {
-                if (q < XR_T + len - 1) {
-                    int r = base + q;
-                    r = r < 0 ? 0 : (r >= n1 ? n1 - 1 : r);
-                    z[q] = __ldg(Z + (long long)r * n2 + ac);
-                }
-            }
-#pragma unroll
-            for (int kk = 0; kk < MAXL; ++kk) {
-                if (kk < len) {
-#pragma unroll
-                    for (int t = 0; t < XR_T; ++t) {
-                        double c;
-                        if (fast) {
-                            c = cf[klo + kk];
-                        } else {
-                            const int it = min(i0 + t, n1 - 1);
-                            c = E.ctab ? __ldg(E.ctab + cls[t] * W + klo + kk)
-                                       : __ldg(E.cst + (long long)(klo + kk) * n1 + it);
-                        }
-                        tmp[t] = fma(c, z[t + kk], tmp[t]);
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int s = 0; s < SO; ++s)
-            if (s == E.s_out)
-#pragma unroll
-                for (int t = 0; t < XR_T; ++t) acc[s][t] = fma(E.scale, tmp[t], acc[s][t]);
-    }
-#pragma unroll
-    for (int s = 0; s < SO; ++s)
-#pragma unroll
-        for (int t = 0; t < XR_T; ++t) red[warp][s][t][lane] = acc[s][t];
-    __syncthreads();
-    // warp w reduces target rows t = w (XR_T = 8 = #warps) for every s
-    {
-        const int t = warp;
-        if (i0 + t < n1 && aval) {
-#pragma unroll
-            for (int s = 0; s < SO; ++s) {
-                double v = 0.0;
-#pragma unroll
-                for (int w = 0; w < 8; ++w) v += red[w][s][t][lane];
-                double* y = Y + s * plane + (long long)(i0 + t) * n2 + a;
-                *y = beta == 0.0 ? v : fma(beta, *y, v);
-            }
-        }
-    }
-}
-
-int launch_xgat_reg(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so, int m,
-                    const uint8_t* xflag, const XgatParams& ep, double* Y, double beta) {
-    const int64_t ctiles = (n2 + 31) / 32;
-    const int64_t rgroups = (n1 + XR_T - 1) / XR_T;
-    const int64_t nb = ctiles * rgroups;
-    if (n1 * n2 >= (1LL << 31) || nb >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
-#define XR(DD, SS) k_xgat_reg<DD, SS><<<(unsigned)nb, 256, 0, P->stream>>>((int)n1, (int)n2, so, m, xflag, ep, Y, beta, (int)ctiles)
-    if (S_out == 1) {
-        if (d == 1) XR(1, 1); else if (d == 2) XR(2, 1); else XR(3, 1);
-    } else {
-        if (d == 1) XR(1, 2); else if (d == 2) XR(2, 2); else XR(3, 2);
-    }
-#undef XR
-    P->launches++;
-    SG_CUDA(cudaGetLastError());
     return SG_OK;
 }
 }  // namespace sg

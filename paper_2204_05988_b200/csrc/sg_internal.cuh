@@ -107,6 +107,7 @@ struct CombEntry {
     double* vals;   // [W][n] device (owned)
     double* st = nullptr;   // stencil format (box lattice of the other factor), owned
     double* ctab = nullptr; // class table [27][W] if translation invariant, owned
+    int64_t nnz = 0;        // structural nonzeros (FLOP count)
 };
 struct Group {                 // terms sharing one spec on the "inner" factor
     int spec;                  // shared spec id (v-spec for lower/x-groups, x-spec for upper)
@@ -178,6 +179,22 @@ struct GraphEntry {
     int64_t nlaunch;
 };
 
+// Device-resident state of the strip solver (strip_solver.cu), one per handle.  The
+// cond_* words mirror the conditional-node values for the uncaptured (host-loop) path.
+struct SolveCtl {
+    int it, mr, have_r, done;        // outer iteration; MR steps on; r current; 0 run / 1 conv / 2 max_iter / 3 non-finite
+    int inner_it, cond_inner, cond_outer, cond_need_r, cond_mr, pad0;
+    double nd, nd_prev, nu2, omega;
+    double dots[4];
+    // cumulative counters (reset by sg_reset_stats)
+    long long outer_iters, inner_iters, need_r_runs, mr_runs, mr_switches;
+    long long inner_breakdowns, inner_maxit, outer_unconverged, outer_nonfinite;
+    long long n_applies, timed_applies;
+    double dof_applied, alg_bytes, alg_flops, apply_ns;
+    unsigned long long t0;
+    int act[64];                     // grid active in the current inner iteration
+};
+
 struct Grid {
     int l1, l2;
     int64_t n1, n2;
@@ -216,65 +233,64 @@ struct sg_problem {
     double* wsH = nullptr;                        // per-target Horner buffers [2][active S-set]
     double* red = nullptr;                        // reduction partials
     double* scal = nullptr;                       // per-grid scalars (BiCGStab)
-    double* hscal = nullptr;                      // pinned host copy
     std::vector<double*> vec;                     // solver vectors
     double* trace_dev = nullptr;
     double* dinv = nullptr;                       // block-Jacobi inverse (solve set)
-    bool use_precond = true;
-    bool use_classes = true;
-    bool use_graphs = true;
-    bool use_brick = true;
-    bool use_reg = true;           // register-coefficient pass kernels
+    bool use_tma = true;           // SG_NO_TMA: pass 2 by the register line sweep k_xfanin
+    bool use_graphs = true;        // SG_NO_GRAPHS: cross-grid applies and strip solves uncaptured
+    sg::SolveCtl* ctl = nullptr;   // device-resident solver state
+    sg::SolveCtl* hctl = nullptr;  // pinned host copy
+    const double* skip = nullptr;  // convergence flag of the grid being applied (kernels exit if != 0)
+    bool capturing = false;        // enqueueing into a strip-solve graph
+    bool in_solve = false;         // applies are counted on the device (inner control kernel)
+    std::vector<cudaStream_t> cap_streams;   // capture streams of nested conditional bodies
+    struct SolveGraph {
+        const double *b, *u;
+        double rtol, inner_rtol;
+        int max_iter, mode, timing;
+        cudaGraphExec_t exec;
+        int64_t l_pre, l_outer, l_need_r, l_mr, l_inner;   // launches per region execution
+    };
+    std::vector<SolveGraph> solve_graphs;
+    std::vector<double> gdof, gbytes, gflops;   // per solve grid (active then coarse): DOF, alg. bytes / flops per apply
     cudaStream_t gstream = nullptr;   // library stream for captured graphs
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;
     std::vector<sg::GraphEntry> graphs;
-    bool use_xfanin = true;        // line-swept x fan-in pass 2 (SG_OLD_XG disables)
-    int xfi_cpt = 1, xfi_seg = 0;
-    bool use_xfi_tma = true;
-    int xft_wc = 0, xft_box_kb = 24;   // TMA tile: forced column groups (SG_XFT_WC), stage box limit (SG_XFT_BOX_KB)
-    int xft_smem_kb = 0;
-    int xft_nst_wide = 3;          // pipeline depth of the wide-box 3D tiles (SG_XFT_NST_WIDE)           // shared-memory budget of the TMA pipeline (SG_XFT_SMEM_KB; 0: 4 stages)
-    bool use_xwhole = true;        // whole-x pass 2 on tiny x lattices (SG_NO_XWHOLE disables)       // TMA-pipelined pass 2 (SG_NO_TMA disables)  // SG_XFI_CPT (columns per lane), SG_XFI_SEG (sweep segment length, 0 auto)
-    std::vector<double*> xfi_itab; // per x-level: interior groups only [3^d][ng_int][W]
-    std::vector<double*> xfi_tab;  // per x-level: class table [3^d][groups][W] of the combined x matrices
+    // pass 2 line sweeps, per x-level: class tables [3^d][groups][W] of the combined x matrices,
+    // interior-group class tables [3^d][ng_int][W] and the interior-class coefficients
+    std::vector<double*> xfi_tab;
+    std::vector<double*> xfi_itab;
     std::vector<std::vector<double>> xfi_cint;
-    std::vector<double*> xw_tab;   // per x-level (tiny lattices): non-null when the whole-x tables exist
-    std::vector<double*> xw_dev;   // per x-level: compact [group][pair] coefficient table (device)
+    // whole-x pass 2 (tiny x-lattices), per x-level: compact [group][pair] coefficient table
+    std::vector<double*> xw_tab;   // non-null when the whole-x tables exist
+    std::vector<double*> xw_dev;
     std::vector<int> xw_np;
-    double* cross_q = nullptr;     // batched cross-grid lower part: stage-0 fan-outs of all v-groups
-    double* cross_h = nullptr;     //   and the Horner results per target and group (even pitch)
+    // batched cross-grid lower part: stage-0 fan-outs of all v-groups and the Horner
+    // results per target and group (even pitch); also used by the batched upper part
+    double* cross_q = nullptr;
+    double* cross_h = nullptr;
     bool cross_batched_tried = false;
     int64_t cross_q_n = 0, cross_h_n = 0;
     bool use_cross_batched = true; // SG_NO_CROSS_BATCH disables
     int outer_mode = 0;            // 0 Richardson + minimal-residual safeguard, 1 plain Richardson, 2 MR always
     int64_t mr_switches = 0;
-    bool use_jobs2 = true;
-    bool use_gather_s2 = true;
-    bool use_rbox = true;          // stencil-form restriction jobs on box lattices (SG_NO_RBOX)     // x-gather producing both dG(1) components per thread (SG_NO_GATHER_S2)         // warp-unit transfer-job kernel (SG_OLD_JOBS: element kernel)
-    bool use_warm = true;          // warm-started block solves (SG_NO_WARM disables)
-    bool warm_valid = false;
-    bool use_vmom = true;          // moment pass 1 (SG_NO_VMOM disables)
-    bool force_vmom = false;       // SG_VMOM: moment pass 1 on every grid
-    bool use_vfan_k = true;        // k-outer pass-1 kernel (SG_NO_VFANK disables)
-    std::vector<int> vm_ok;        // per v-level: moment tables verified
-    std::vector<double*> vm_tab;   // per v-level: [3^d][10][W] shifted-moment class tables
-    std::vector<std::vector<double>> vm_int;   // per v-level: interior class [10][15]
-    std::vector<int*> vm_blist;    // per v-level: boundary v-nodes
+    // moment pass 1 (vmoment.cu), per v-level
+    std::vector<int> vm_ok;        // moment tables verified
+    std::vector<double*> vm_tab;   // [3^d][10][W] shifted-moment class tables
+    std::vector<std::vector<double>> vm_int;   // interior class [10][15]
+    std::vector<int*> vm_blist;    // boundary v-nodes
     std::vector<int> vm_nb;
     std::vector<int> vm_slot;      // interior group position -> monomial slot
+    int64_t vm_tab_n = 0;          // doubles of one level's moment class table (byte count)
     int vm_nchi = 0;               // boundary-only groups handled as chi-weighted moments (0: stencil kernel)
-    int vm_chax[6] = {0}, vm_chkeep[6] = {0};   // per x-level (tiny lattices): [group][row][k] coefficients   // per x-level: interior-class coefficients [12][15]
-    bool use_fused = false;        // opt-in fused whole-x kernel (SG_FUSED)
-    int xfirst_mode = 0;           // 0 auto (n1 > n2), 1 never, 2 always (tests)
-    int* egrp_dev = nullptr;       // group index of every diag gather entry (fused kernels)
-    int egrp_n = 0;
+    int vm_chax[6] = {0}, vm_chkeep[6] = {0};
     // instrumentation
-    int64_t n_applies = 0, dof_applied = 0, launches = 0, outer_iters = 0, inner_iters = 0;
-    bool timing = false;
+    // (host-side counters of applies issued outside the strip solver; the solver counts on the device)
+    int64_t n_applies = 0, dof_applied = 0, launches = 0;
+    bool timing = false;           // globaltimer stamps around every strip-operator apply (k_tstamp)
     bool verbose = false;
-    std::vector<cudaEvent_t> ev_pool;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pairs;
-    double kern_ms = 0; int64_t kern_launches = 0; double kern_bytes = 0; double kern_flops = 0;
+    // per factor/level/spec structural nonzeros (|a_ij| > 1e-12 max|a|) for the FLOP count
+    std::vector<std::vector<int64_t>> nnz_x, nnz_v;
 };
 
 namespace sg {
@@ -294,21 +310,10 @@ int launch_ell_to_stencil(sg_problem* P, int64_t n, int W, const int32_t* cols, 
                           const StencilOff& so, double* out);
 int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, const uint8_t* xflag,
                    const VfanParams& vp, const double* X, int64_t opitch = 0);
-int launch_vfan_k(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, const uint8_t* xflag,
-                  const VfanParams& vp, const double* X, int64_t opitch = 0);
 int launch_xgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
                    const uint8_t* xflag, const XgatParams& ep, double* Y, double beta, int m = 0);
 int class_compress(sg_problem* P, const Factor& f, int l, const double* st, double** ctab);
 int launch_jobs(sg_problem* P, std::vector<Job>& jobs);
-int launch_vfan_reg(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, const uint8_t* xflag,
-                    const VfanParams& vp, const double* X);
-int launch_xgat_reg(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so, int m,
-                    const uint8_t* xflag, const XgatParams& ep, double* Y, double beta);
-int launch_xgat_brick3(sg_problem* P, int S_out, int64_t n1, int64_t n2, int m, const uint8_t* xflag,
-                       const XgatParams& ep, double* Y, double beta);
-int launch_fused_wx(sg_problem* P, int dv, int dx, int S, int64_t n1, int64_t n2, const StencilOff& sov,
-                    const StencilOff& sox, int mx, const uint8_t* xflag, const VfanParams& vp, const XgatParams& ep,
-                    const int* egrp_dev, const double* X, double* Y);
 int launch_vgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
                    const XgatParams& ep, double* Y, double beta, const uint8_t* xflag = nullptr);
 int launch_xfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, int m,
@@ -327,11 +332,29 @@ int launch_vmom(sg_problem* P, int l2, int64_t nrows, int64_t n2, int64_t pitch,
 int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pitch, const double* Z,
                       int64_t gstride, double* Y);
 // solver.cu
-int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y);
-int pass1_vgroups(sg_problem* P, int l1, int l2, const double* X, double* const* outs, int64_t pitch);
+int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y, const double* skip = nullptr);
+int apply_cost(sg_problem* P, const Grid& g, double* bytes, double* flops);
+int count_nnz(sg_problem* P);
+int pass1_vgroups(sg_problem* P, int l1, int l2, const double* X, double* const* outs, int64_t pitch,
+                  double* fbytes = nullptr);
+int apply_cross_prepare(sg_problem* P);
 int apply_cross(sg_problem* P, const std::vector<Term>* terms_override, const double* Tb, int S_out, int S_in,
                 const double* X, double* Y);
 int64_t set_size(const sg_problem* P, int set, int S);
 int build_block_jacobi(sg_problem* P);
+// strip_solver.cu
+int solver_init(sg_problem* P);
+int solver_destroy(sg_problem* P);
+int sync_stats(sg_problem* P);
+int reset_device_stats(sg_problem* P);
+int combine(sg_problem* P, int S, const double* dhat_a, const double* dhat_c, double* du);
+int solve_strip(sg_problem* P, const double* b, double* u, double rtol, double inner_rtol, int max_iter, int* iters,
+                double* last);
+int step(sg_problem* P, int j0, int nsteps, double* trace_dev, double rtol, double inner_rtol);
+// solver.cu (data)
+int rhs(sg_problem* P, int j, const double* trace, double* b);
+int trace_of(sg_problem* P, const double* u, double* tr);
+int interp_u0(sg_problem* P, double* u);
+__global__ void k_tstamp(SolveCtl* c, const double* skip, int phase, double bytes, double flops);
 int prepare_stencils(sg_problem* P);
 }  // namespace sg

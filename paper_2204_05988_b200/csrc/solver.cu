@@ -20,39 +20,16 @@ int64_t set_size(const sg_problem* P, int set, int S) {
 
 static inline int64_t gsize(const Grid& g) { return g.n1 * g.n2; }
 
-// ------------------------------------------------------------------ timing
-static int timed_begin(sg_problem* P, cudaEvent_t* e0) {
-    if (!P->timing) return SG_OK;
-    SG_CUDA(cudaEventCreate(e0));
-    SG_CUDA(cudaEventRecord(*e0, P->stream));
-    return SG_OK;
-}
-static int timed_end(sg_problem* P, cudaEvent_t e0, double bytes, double flops, int nl) {
-    if (!P->timing) return SG_OK;
-    cudaEvent_t e1;
-    SG_CUDA(cudaEventCreate(&e1));
-    SG_CUDA(cudaEventRecord(e1, P->stream));
-    P->ev_pairs.push_back({e0, e1});
-    P->kern_launches += nl;
-    P->kern_bytes += bytes;
-    P->kern_flops += flops;
-    return SG_OK;
-}
-
-// pass-2 dispatcher: 2x2x2 register bricks on 3D box x-lattices, band kernel otherwise
+// generic pass 2 on box x-lattices (band kernel over the stencil-format matrices)
 static int xgather(sg_problem* P, const Grid& g, const XgatParams& ep, double* Y, double beta) {
     const Level& Lx = P->fx.lev[g.l1];
-    if (P->fx.d == 3 && P->use_brick && Lx.m >= 3)
-        return launch_xgat_brick3(P, P->S, g.n1, g.n2, Lx.m, Lx.bflag, ep, Y, beta);
-    if (P->use_reg) {
-        int rc = launch_xgat_reg(P, P->fx.d, P->S, g.n1, g.n2, Lx.so, Lx.m, Lx.bflag, ep, Y, beta);
-        if (rc != SG_ERR_UNSUPPORTED) return rc;
-    }
     return launch_xgat_st(P, P->fx.d, P->S, g.n1, g.n2, Lx.so, Lx.bflag, ep, Y, beta, Lx.m);
 }
 
-// algorithmic FLOPs of one strip-operator apply on grid g (2 per multiply-add):
-// interior groups on every x-row, boundary-only (face) groups on boundary x-rows only
+// Algorithmic FLOPs of one strip-operator apply on grid g (2 per multiply-add), counted on the
+// structural nonzeros of the factor matrices (count_nnz): pass 1 applies B_b to every used x-row
+// (interior groups: all S*n1 rows, boundary-only face groups: the S*nbnd x-boundary rows),
+// pass 2 applies every combined x matrix C_b^{ss'} to all n2 columns.
 static double diag_flops(const sg_problem* P, const Grid& g) {
     const int S = P->S;
     const int64_t nb1 = P->fx.lev[g.l1].nbnd;
@@ -60,21 +37,23 @@ static double diag_flops(const sg_problem* P, const Grid& g) {
     for (int o = 0; o < (int)P->vorder.size(); ++o) {
         const Group& gr = P->vgroups[P->vorder[o]];
         const double rows = gr.bonly ? (double)nb1 : (double)g.n1;
-        const double ne = (double)gr.comb[g.l1].size();
-        f += 2.0 * rows * g.n2 * (S * P->fv.W + ne * P->fx.W);
+        f += 2.0 * S * rows * (double)P->nnz_v[g.l2][gr.spec];
+        for (const auto& ce : gr.comb[g.l1]) f += 2.0 * (double)ce.nnz * (double)g.n2;
     }
     return f;
 }
 
 static bool l_has_xfi(const sg_problem* P, int l1) {
-    return l1 < (int)P->xfi_tab.size() && P->xfi_tab[l1] != nullptr &&
+    return P->use_tma && l1 < (int)P->xfi_tab.size() && P->xfi_tab[l1] != nullptr &&
            ((P->fx.d == 3 && P->ng_int == 10) || (P->fx.d == 2 && P->ng_int == 6)) && P->fx.lev[l1].m >= 3;
 }
 
 // pass 1 of the per-grid operator on grid (l1, l2): Z_o = (Id x Id x B_o) X for every v-group o
 // (vorder; boundary-only groups on x-boundary rows only), written with row pitch `pitch`
-int pass1_vgroups(sg_problem* P, int l1, int l2, const double* X, double* const* outs, int64_t pitch) {
+int pass1_vgroups(sg_problem* P, int l1, int l2, const double* X, double* const* outs, int64_t pitch, double* fbytes) {
     const int S = P->S;
+    double fb_dummy = 0.0;
+    if (!fbytes) fbytes = &fb_dummy;
     const Level& Lx = P->fx.lev[l1];
     const Level& Lv = P->fv.lev[l2];
     const int64_t n1 = Lx.n, n2 = Lv.n;
@@ -89,10 +68,11 @@ int pass1_vgroups(sg_problem* P, int l1, int l2, const double* X, double* const*
             vp.out[o] = outs[o];
         }
         int rc = SG_ERR_UNSUPPORTED;
-        const bool vmom_here = P->force_vmom || P->fv.d == 2 || n1 < 64;
-        if (!P->use_reg && P->use_vmom && vmom_here) {
+        const bool vmom_here = P->fv.d == 2 || n1 < 64;
+        if (vmom_here) {
             // interior groups by shifted moments, boundary-only (face) groups by the stencil kernel
             rc = launch_vmom(P, l2, (int64_t)S * n1, n2, pitch, X, vp.out, Lx.bflag, n1);
+            if (rc == SG_OK) *fbytes += 8.0 * (double)P->vm_tab_n;   // class tables
             if (rc == SG_OK && nb > P->ng_int && P->vm_nchi == 0) {
                 VfanParams vb;
                 vb.ng = nb - P->ng_int;
@@ -102,12 +82,13 @@ int pass1_vgroups(sg_problem* P, int l1, int l2, const double* X, double* const*
                     vb.out[o] = vp.out[P->ng_int + o];
                 }
                 rc = launch_vfan_st(P, P->fv.d, S, n1, n2, Lv.so, Lx.bflag, vb, X, pitch);
+                *fbytes += 8.0 * vb.ng * P->fv.W * (double)n2;   // per-column stencil coefficients
             }
         }
-        if (rc == SG_ERR_UNSUPPORTED && P->use_vfan_k && !P->use_reg)
-            rc = launch_vfan_k(P, P->fv.d, S, n1, n2, Lv.so, Lx.bflag, vp, X, pitch);
-        if (rc == SG_ERR_UNSUPPORTED && P->use_reg) rc = launch_vfan_reg(P, P->fv.d, S, n1, n2, Lv.so, Lx.bflag, vp, X);
-        if (rc == SG_ERR_UNSUPPORTED) rc = launch_vfan_st(P, P->fv.d, S, n1, n2, Lv.so, Lx.bflag, vp, X, pitch);
+        if (rc == SG_ERR_UNSUPPORTED) {
+            rc = launch_vfan_st(P, P->fv.d, S, n1, n2, Lv.so, Lx.bflag, vp, X, pitch);
+            *fbytes += 8.0 * nb * P->fv.W * (double)n2;
+        }
         return rc;
     }
     if (pitch != n2) return SG_ERR_UNSUPPORTED;
@@ -119,6 +100,7 @@ int pass1_vgroups(sg_problem* P, int l1, int l2, const double* X, double* const*
             fl.out[o] = outs[b0 + o];
         }
         SG_TRY(launch_fanout(P, 1, P->fv.W, S, n1, n2, n2, Lv.cols, X, fl));
+        *fbytes += (8.0 * fl.no + 4.0) * P->fv.W * (double)n2;   // ELL values + pattern
     }
     return SG_OK;
 }
@@ -127,12 +109,9 @@ int pass1_vgroups(sg_problem* P, int l1, int l2, const double* X, double* const*
 // Y = sum_o C_o Z_o with the line-swept kernels; SG_ERR_UNSUPPORTED if they do not cover it
 static int pass2_fast(sg_problem* P, int l1, int l2, const double* Z, int64_t pitch, int64_t gstr, double* Y) {
     const int64_t n1 = P->fx.lev[l1].n, n2 = P->fv.lev[l2].n;
-    if (P->fx.kind != SG_MESH_BOX || P->fv.kind != SG_MESH_BOX || P->S != 1 || !P->use_xfanin || P->use_brick ||
-        P->use_reg)
-        return SG_ERR_UNSUPPORTED;
-    int rc = SG_ERR_UNSUPPORTED;
-    if (P->use_xwhole) rc = launch_xwhole(P, l1, n1, n2, pitch, Z, gstr, Y);
-    if (rc == SG_ERR_UNSUPPORTED && P->use_xfi_tma && (pitch & 1) == 0 && l_has_xfi(P, l1))
+    if (P->fx.kind != SG_MESH_BOX || P->fv.kind != SG_MESH_BOX || P->S != 1) return SG_ERR_UNSUPPORTED;
+    int rc = launch_xwhole(P, l1, n1, n2, pitch, Z, gstr, Y);
+    if (rc == SG_ERR_UNSUPPORTED && (pitch & 1) == 0 && l_has_xfi(P, l1))
         rc = launch_xfanin_tma(P, l1, n1, n2, pitch, Z, gstr, Y);
     if (rc == SG_ERR_UNSUPPORTED && pitch == n2) rc = launch_xfanin(P, l1, n1, n2, Z, gstr, Y, 0.0);
     return rc;
@@ -140,107 +119,20 @@ static int pass2_fast(sg_problem* P, int l1, int l2, const double* Z, int64_t pi
 
 // ------------------------------------------------ diagonal block (one grid)
 // Y = sum_t T_t (x) A_t (x) B_t X, grouped by the v-spec b:
-//   Z_b = (Id x Id x B_b) X           (fanout along v, one read of X per 4 b's)
+//   Z_b = (Id x Id x B_b) X           (pass 1, along v)
 //   Y   = sum_b sum_{s,s'} (e_s e_s'^T (x) C_b^{ss'} (x) Id) Z_b,  C_b^{ss'} = sum_{t in b} T_t[s,s'] A_t
 // (application order of l.516-532 with S^(2) first, the intermediates stay on
-// the grid's own level because l = l').
-int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
+// the grid's own level because l = l').  *fbytes: factor data the launched kernels read.
+static int apply_diag_impl(sg_problem* P, const Grid& g, const double* X, double* Y, double* fbytes) {
     const int S = P->S;
     const int64_t n = gsize(g);
     const Level& Lx = P->fx.lev[g.l1];
-    const Level& Lv = P->fv.lev[g.l2];
     const int nb = (int)P->vorder.size();
-    if ((size_t)nb * S * n > P->wsZ_n) {
-        set_error("apply_diag: workspace too small");
-        return SG_ERR_STATE;
-    }
-    cudaEvent_t e0 = nullptr;
-    SG_TRY(timed_begin(P, &e0));
-    int64_t l0 = P->launches;
     const bool vbox = P->fv.kind == SG_MESH_BOX && nb <= MAXG;
     const bool xbox = P->fx.kind == SG_MESH_BOX;
-    // ---- fused single pass when the whole x factor of a 32-column tile fits in shared memory
-    if (vbox && xbox && P->use_fused) {
-        VfanParams vp;
-        vp.ng = nb;
-        vp.ng_int = P->ng_int;
-        XgatParams ep;
-        ep.ne = 0;
-        std::vector<int> eg;
-        bool fits = true;
-        for (int o = 0; o < nb; ++o) {
-            const Group& gr = P->vgroups[P->vorder[o]];
-            vp.vst[o] = Lv.fst[gr.spec];
-            vp.out[o] = nullptr;
-            for (const auto& ce : gr.comb[g.l1]) {
-                if (ep.ne == MAX_ENTRIES) {
-                    fits = false;
-                    break;
-                }
-                ep.e[ep.ne++] = {nullptr, ce.st, ce.s_out, ce.s_in, gr.bonly ? 1 : 0, 1.0, ce.ctab};
-                eg.push_back(o);
-            }
-        }
-        if (fits && (int)eg.size() == P->egrp_n) {
-            int rc = launch_fused_wx(P, P->fv.d, P->fx.d, S, g.n1, g.n2, Lv.so, Lx.so, Lx.m, Lx.bflag, vp, ep,
-                                     P->egrp_dev, X, Y);
-            if (rc == SG_OK) {
-                P->n_applies++;
-                P->dof_applied += S * n;
-                double bytes = 16.0 * S * n + (8.0 * nb + 4.0) * (double)(P->fv.W * g.n2) +
-                               (8.0 * ep.ne) * (double)(P->fx.W * g.n1);
-                SG_TRY(timed_end(P, e0, bytes, diag_flops(P, g), (int)(P->launches - l0)));
-                return SG_OK;
-            }
-            if (rc != SG_ERR_UNSUPPORTED) return rc;
-        }
-    }
-    // ---- x-first two-pass order for grids with a large x and a small v factor:
-    // U_a = (Id x A_a x Id) X for every x-group a, then Y = sum_a (Id x D_a) U_a along v.
-    // The x-halo (lexicographic offsets up to m^2 rows) then falls on the single
-    // input X instead of on every intermediate.
-    const int nxg = (int)P->xorder.size();
-    if (vbox && xbox && nxg <= MAXG && (size_t)nxg * S * n <= P->wsZ_n &&
-        (P->xfirst_mode == 2 || (P->xfirst_mode == 0 && g.n1 > g.n2))) {
-        XfanParams fp;
-        fp.ng = nxg;
-        fp.ng_int = P->nxg_int;
-        int64_t nnz_e = 0;
-        XgatParams ep;
-        ep.ne = 0;
-        bool fits = true;
-        for (int o = 0; o < nxg; ++o) {
-            const Group& gr = P->xgroups[P->xorder[o]];
-            fp.cst[o] = Lx.fst[gr.spec];
-            fp.ctab[o] = Lx.fcls.size() > (size_t)gr.spec ? Lx.fcls[gr.spec] : nullptr;
-            fp.out[o] = P->wsZ + (int64_t)o * S * n;
-            for (const auto& ce : gr.comb[g.l2]) {
-                if (ep.ne == MAX_ENTRIES) {
-                    fits = false;
-                    break;
-                }
-                ep.e[ep.ne++] = {fp.out[o], ce.st, ce.s_out, ce.s_in, gr.bonly ? 1 : 0, 1.0, nullptr};
-                nnz_e++;
-            }
-        }
-        if (fits) {
-            int rc = launch_xfan_st(P, P->fx.d, S, g.n1, g.n2, Lx.so, Lx.m, Lx.bflag, fp, X);
-            if (rc == SG_OK) {
-                SG_TRY(launch_vgat_st(P, P->fv.d, S, g.n1, g.n2, Lv.so, ep, Y, 0.0, Lx.bflag));
-                P->n_applies++;
-                P->dof_applied += S * n;
-                double bytes = 16.0 * S * n + (8.0 * nnz_e + 4.0) * (double)(P->fv.W * g.n2) +
-                               (8.0 * nxg + 4.0) * (double)(P->fx.W * g.n1);
-                SG_TRY(timed_end(P, e0, bytes, diag_flops(P, g), (int)(P->launches - l0)));
-                return SG_OK;
-            }
-            if (rc != SG_ERR_UNSUPPORTED) return rc;
-        }
-    }
     // ---- pass 1: Z_b = (Id x Id x B_b) X for every v-group b (interior groups first)
     // (TMA pass 2 reads the intermediates with an even row pitch)
-    const bool tma2 = vbox && xbox && P->use_xfanin && P->use_xfi_tma && !P->use_brick && !P->use_reg && S == 1 &&
-                      l_has_xfi(P, g.l1);
+    const bool tma2 = vbox && xbox && S == 1 && l_has_xfi(P, g.l1);
     const int64_t pitch = tma2 ? g.n2 + (g.n2 & 1) : g.n2;
     const int64_t gstr = (int64_t)S * g.n1 * pitch;
     if ((size_t)nb * gstr > P->wsZ_n) {
@@ -250,13 +142,12 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
     {
         std::vector<double*> outs(nb);
         for (int o = 0; o < nb; ++o) outs[o] = P->wsZ + (int64_t)o * gstr;
-        SG_TRY(pass1_vgroups(P, g.l1, g.l2, X, outs.data(), pitch));
+        SG_TRY(pass1_vgroups(P, g.l1, g.l2, X, outs.data(), pitch, fbytes));
     }
     // ---- pass 2: Y = sum_b sum_{s,s'} (e_s e_s'^T (x) C_b^{ss'} (x) Id) Z_b
-    int64_t nnz_x = 0;
     double beta = 0.0;
     int rcx = SG_ERR_UNSUPPORTED;
-    if (vbox && xbox && P->use_xfanin && P->use_xwhole && !P->use_brick && !P->use_reg && S == 1) {
+    if (vbox && xbox && S == 1) {
         rcx = launch_xwhole(P, g.l1, g.n1, g.n2, pitch, P->wsZ, gstr, Y);
         if (rcx != SG_OK && rcx != SG_ERR_UNSUPPORTED) return rcx;
     }
@@ -268,12 +159,14 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
             return SG_ERR_STATE;
         }
     }
-    if (rcx != SG_OK && xbox && P->use_xfanin && !P->use_brick && !P->use_reg) {
+    if (rcx != SG_OK && xbox) {
         rcx = launch_xfanin(P, g.l1, g.n1, g.n2, P->wsZ, (int64_t)S * n, Y, 0.0);
         if (rcx != SG_OK && rcx != SG_ERR_UNSUPPORTED) return rcx;
     }
     if (rcx == SG_OK) {
-        for (int o = 0; o < nb; ++o) nnz_x += (int64_t)P->vgroups[P->vorder[o]].comb[g.l1].size();
+        int ncls = 1;
+        for (int q = 0; q < P->fx.d; ++q) ncls *= 3;
+        *fbytes += 8.0 * ncls * nb * P->fx.W;   // class tables of the line-swept kernels
     } else if (xbox) {
         XgatParams ep;
         ep.ne = 0;
@@ -286,13 +179,14 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
                     ep.ne = 0;
                 }
                 ep.e[ep.ne++] = {P->wsZ + (int64_t)o * S * n, ce.st, ce.s_out, ce.s_in, gr.bonly ? 1 : 0, 1.0, ce.ctab};
-                nnz_x++;
+                *fbytes += ce.ctab ? 8.0 * 27 * P->fx.W : 8.0 * P->fx.W * (double)g.n1;
             }
         }
         SG_TRY(xgather(P, g, ep, Y, beta));
     } else {
         EntryList el;
         el.ne = 0;
+        *fbytes += 4.0 * P->fx.W * (double)g.n1;   // ELL pattern
         for (int o = 0; o < nb; ++o) {
             for (const auto& ce : P->vgroups[P->vorder[o]].comb[g.l1]) {
                 if (el.ne == MAX_ENTRIES) {
@@ -301,18 +195,97 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y) {
                     el.ne = 0;
                 }
                 el.e[el.ne++] = {P->wsZ + (int64_t)o * S * n, ce.vals, 1.0, ce.s_out, ce.s_in};
-                nnz_x++;
+                *fbytes += 8.0 * P->fx.W * (double)g.n1;
             }
         }
         SG_TRY(launch_gather(P, 0, P->fx.W, S, g.n1, g.n2, g.n1, Lx.cols, el, Y, beta));
     }
-    P->n_applies++;
-    P->dof_applied += S * n;
-    // algorithmic bytes: read X, write Y, factor matrices (values + pattern)
-    double bytes = 16.0 * S * n + (8.0 * nb + 4.0) * (double)(P->fv.W * g.n2) +
-                   (8.0 * nnz_x + 4.0) * (double)(P->fx.W * g.n1);
-    SG_TRY(timed_end(P, e0, bytes, diag_flops(P, g), (int)(P->launches - l0)));
     return SG_OK;
+}
+
+// One strip-operator apply.  skip: the grid's convergence flag inside the batched block solver
+// (every kernel of the apply exits when it is non-zero).  Timing mode brackets the apply with
+// device timestamps (k_tstamp) that also accumulate its algorithmic bytes (read X + write Y +
+// the factor data its kernels read) and FLOPs (structural nonzeros).
+int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y, const double* skip) {
+    const int S = P->S;
+    const int64_t n = gsize(g);
+    if (P->timing) {
+        k_tstamp<<<1, 1, 0, P->stream>>>(P->ctl, skip, 0, 0.0, 0.0);
+        P->launches++;
+    }
+    P->skip = skip;
+    double fbytes = 0.0;
+    const int rc = apply_diag_impl(P, g, X, Y, &fbytes);
+    P->skip = nullptr;
+    if (rc != SG_OK) return rc;
+    if (P->timing) {
+        k_tstamp<<<1, 1, 0, P->stream>>>(P->ctl, skip, 1, 16.0 * S * (double)n + fbytes, diag_flops(P, g));
+        P->launches++;
+        SG_CUDA(cudaGetLastError());
+    }
+    if (!P->in_solve) {   // inside the strip solver the device counts the applies
+        P->n_applies++;
+        P->dof_applied += S * n;
+    }
+    return SG_OK;
+}
+
+// Structural nonzeros (|a_ij| > 1e-12 max |a|) of every factor matrix and combined x matrix,
+// for the FLOP count of diag_flops (setup time).
+__global__ void k_absmax(int64_t n, const double* __restrict__ v, unsigned long long* out) {
+    unsigned long long m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(v[i]));
+        m = b > m ? b : m;
+    }
+    atomicMax(out, m);
+}
+__global__ void k_count_nz(int64_t n, const double* __restrict__ v, const unsigned long long* mx,
+                           unsigned long long* out) {
+    const double th = 1e-12 * __longlong_as_double((long long)*mx);
+    unsigned long long c = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        c += fabs(v[i]) > th;
+    atomicAdd(out, c);
+}
+static int nnz_of(sg_problem* P, const double* vals, int64_t n, unsigned long long* dbuf, int64_t* out) {
+    if (!vals) {
+        *out = 0;
+        return SG_OK;
+    }
+    SG_CUDA(cudaMemsetAsync(dbuf, 0, 2 * sizeof(unsigned long long), P->stream));
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    k_absmax<<<std::max(blocks, 1), 256, 0, P->stream>>>(n, vals, dbuf);
+    k_count_nz<<<std::max(blocks, 1), 256, 0, P->stream>>>(n, vals, dbuf, dbuf + 1);
+    P->launches += 2;
+    unsigned long long h[2];
+    SG_CUDA(cudaMemcpyAsync(h, dbuf, sizeof(h), cudaMemcpyDeviceToHost, P->stream));
+    SG_CUDA(cudaStreamSynchronize(P->stream));
+    *out = (int64_t)h[1];
+    return SG_OK;
+}
+int count_nnz(sg_problem* P) {
+    unsigned long long* dbuf;
+    SG_CUDA(cudaMalloc(&dbuf, 2 * sizeof(unsigned long long)));
+    int rc = SG_OK;
+    for (int which = 0; which < 2 && rc == SG_OK; ++which) {
+        Factor& f = which == 0 ? P->fx : P->fv;
+        auto& tab = which == 0 ? P->nnz_x : P->nnz_v;
+        tab.assign(P->F + 1, std::vector<int64_t>(f.specs.size(), 0));
+        for (int l = 1; l <= P->F && rc == SG_OK; ++l)
+            for (size_t sp = 0; sp < f.specs.size() && rc == SG_OK; ++sp)
+                if (sp < f.lev[l].fm.size())
+                    rc = nnz_of(P, f.lev[l].fm[sp], f.lev[l].n * f.W, dbuf, &tab[l][sp]);
+    }
+    for (auto& gr : P->vgroups)
+        for (int l = 1; l <= P->F && rc == SG_OK; ++l)
+            for (auto& ce : gr.comb[l]) {
+                rc = nnz_of(P, ce.vals, P->fx.lev[l].n * P->fx.W, dbuf, &ce.nnz);
+                if (rc != SG_OK) break;
+            }
+    cudaFree(dbuf);
+    return rc;
 }
 
 // stencil offsets / boundary flags / stencil-format matrices for box lattices
@@ -397,8 +370,7 @@ int prepare_stencils(sg_problem* P) {
             for (auto& g : P->xgroups) SG_TRY(ensure_fst(P->fx, g.spec, l));
             Level& L = P->fx.lev[l];
             L.fcls.assign(P->fx.specs.size(), nullptr);
-            if (P->use_classes)
-                for (size_t sp = 0; sp < P->fx.specs.size(); ++sp)
+            for (size_t sp = 0; sp < P->fx.specs.size(); ++sp)
                     if (L.fst.size() > sp && L.fst[sp]) SG_TRY(class_compress(P, P->fx, l, L.fst[sp], &L.fcls[sp]));
         }
         if (P->fv.kind == SG_MESH_BOX) {
@@ -426,19 +398,10 @@ int prepare_stencils(sg_problem* P) {
                 for (auto& ce : g.comb[l]) {
                     SG_CUDA(cudaMalloc(&ce.st, sizeof(double) * P->fx.W * L.n));
                     SG_TRY(launch_ell_to_stencil(P, L.n, P->fx.W, L.cols, ce.vals, L.so, ce.st));
-                    if (P->use_classes) SG_TRY(class_compress(P, P->fx, l, ce.st, &ce.ctab));
+                    SG_TRY(class_compress(P, P->fx, l, ce.st, &ce.ctab));
                 }
             }
         }
-    }
-    // group index of every diagonal gather entry (same on every level)
-    {
-        std::vector<int> eg;
-        for (int o = 0; o < (int)P->vorder.size(); ++o)
-            for (size_t q = 0; q < P->vgroups[P->vorder[o]].comb[1].size(); ++q) eg.push_back(o);
-        P->egrp_n = (int)std::min<size_t>(eg.size(), MAX_ENTRIES);
-        SG_CUDA(cudaMalloc(&P->egrp_dev, sizeof(int) * MAX_ENTRIES));
-        SG_CUDA(cudaMemcpy(P->egrp_dev, eg.data(), sizeof(int) * P->egrp_n, cudaMemcpyHostToDevice));
     }
     SG_TRY(prepare_xfanin(P));
     SG_TRY(prepare_vmom(P));
@@ -463,14 +426,18 @@ static int cross_lower_batched(sg_problem* P, const double* X, double* Y);
 // chains per group); it is captured once per (X, Y, Tb) into a CUDA graph on the
 // library's own stream and replayed, which removes the per-launch CPU cost
 // (dominant on the 2D configurations).
+int apply_cross_prepare(sg_problem* P) {
+    if (P->cross_batched_tried) return SG_OK;
+    int rc = cross_lower_batched(P, nullptr, nullptr);   // allocation only (never inside a capture)
+    if (rc != SG_OK && rc != SG_ERR_UNSUPPORTED) return rc;
+    P->cross_batched_tried = true;
+    return SG_OK;
+}
+
 int apply_cross(sg_problem* P, const std::vector<Term>* /*unused*/, const double* Tb, int S_out, int S_in,
                 const double* X, double* Y) {
-    if (!P->cross_batched_tried && !Tb) {
-        int rc = cross_lower_batched(P, nullptr, nullptr);   // allocation only (never inside a capture)
-        if (rc != SG_OK && rc != SG_ERR_UNSUPPORTED) return rc;
-        P->cross_batched_tried = true;
-    }
-    if (!P->use_graphs) return apply_cross_impl(P, Tb, S_out, S_in, X, Y);
+    SG_TRY(apply_cross_prepare(P));
+    if (!P->use_graphs || P->capturing) return apply_cross_impl(P, Tb, S_out, S_in, X, Y);
     GraphKey key;
     key.X = X;
     key.Y = Y;
@@ -521,8 +488,7 @@ int apply_cross(sg_problem* P, const std::vector<Term>* /*unused*/, const double
 // Memory: Q0 = stage-0 fan-outs of every group at every source (natural pitch), H = Horner
 // results of every group at every target (even pitch, TMA-readable), both allocated once.
 static int cross_lower_batched(sg_problem* P, const double* X, double* Y) {
-    if (!P->use_cross_batched || P->S != 1 || P->fx.kind != SG_MESH_BOX || P->fv.kind != SG_MESH_BOX || P->fx.d < 2 ||
-        !P->use_xfanin || P->use_brick || P->use_reg)
+    if (!P->use_cross_batched || P->S != 1 || P->fx.kind != SG_MESH_BOX || P->fv.kind != SG_MESH_BOX || P->fx.d < 2)
         return SG_ERR_UNSUPPORTED;
     const auto& A = P->active;
     const int ng = (int)A.size();
@@ -535,9 +501,9 @@ static int cross_lower_batched(sg_problem* P, const double* X, double* Y) {
     // every target must be covered by the fast gathers
     for (int p = 1; p <= ng; ++p) {
         const int m = P->fx.lev[p].m;
-        const bool whole = P->use_xwhole && ((P->fx.d == 3 && m == 3) || (P->fx.d == 2 && (m == 3 || m == 5))) &&
+        const bool whole = ((P->fx.d == 3 && m == 3) || (P->fx.d == 2 && (m == 3 || m == 5))) &&
                            nga <= 16 && p < (int)P->xfi_tab.size() && P->xfi_tab[p];
-        if (!whole && (p == 1 || !(P->use_xfi_tma && l_has_xfi(P, p)))) return SG_ERR_UNSUPPORTED;
+        if (!whole && (p == 1 || !l_has_xfi(P, p))) return SG_ERR_UNSUPPORTED;
     }
     std::vector<int64_t> qo(ng + 2, 0), ho(ng + 2, 0);
     for (int p = 1; p <= ng; ++p) {
@@ -969,581 +935,6 @@ static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in
     return SG_OK;
 }
 
-// ------------------------------------------------------- segmented vectors
-struct SegTab {
-    int nseg;
-    int64_t off[MAX_SEG + 1];
-    int blk[MAX_SEG + 1];
-};
-constexpr int SEG_CHUNK = 2048;
-
-static SegTab make_segs(const std::vector<int64_t>& offs) {   // offs: nseg+1 element offsets
-    SegTab t;
-    t.nseg = (int)offs.size() - 1;
-    int b = 0;
-    for (int i = 0; i <= t.nseg; ++i) {
-        t.off[i] = offs[i];
-        t.blk[i] = b;
-        if (i < t.nseg) b += (int)((offs[i + 1] - offs[i] + SEG_CHUNK - 1) / SEG_CHUNK);
-    }
-    return t;
-}
-
-__device__ inline int seg_of(const SegTab& t, int blk) {
-    int g = 0;
-    while (g + 1 < t.nseg && t.blk[g + 1] <= blk) ++g;
-    return g;
-}
-
-// per-grid scalars: [0] rho [1] alpha [2] omega [3] bnorm2 [4] rnorm2 [5] conv [6] r0v [7] ts [8] tt [9] rr
-constexpr int NSC = 10;
-
-// partial[blk*K + j] = sum over the block's chunk of a_j * b_j
-template <int K>
-__global__ void k_seg_dot(SegTab t, const double* a0, const double* b0, const double* a1, const double* b1,
-                          double* partial, const double* a2 = nullptr, const double* b2 = nullptr,
-                          const double* scal = nullptr) {
-    __shared__ double sh[K][8];
-    const int g = seg_of(t, blockIdx.x);
-    if (scal && scal[g * NSC + 5] != 0.0) {   // converged grid: its scalars are frozen
-        if (threadIdx.x < K) partial[(int64_t)blockIdx.x * K + threadIdx.x] = 0.0;
-        return;
-    }
-    const int64_t lo = t.off[g] + (int64_t)(blockIdx.x - t.blk[g]) * SEG_CHUNK;
-    const int64_t hi = min(lo + SEG_CHUNK, t.off[g + 1]);
-    double s[K];
-    for (int j = 0; j < K; ++j) s[j] = 0.0;
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        s[0] += a0[i] * b0[i];
-        if (K > 1) s[1] += a1[i] * b1[i];
-        if (K > 2) s[2] += a2[i] * b2[i];
-    }
-    for (int j = 0; j < K; ++j) {
-        double v = s[j];
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if ((threadIdx.x & 31) == 0) sh[j][threadIdx.x >> 5] = v;
-    }
-    __syncthreads();
-    if (threadIdx.x < K) {
-        double v = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += sh[threadIdx.x][w];
-        partial[(int64_t)blockIdx.x * K + threadIdx.x] = v;
-    }
-}
-
-// reduce partials of each segment into scal[g*NSC + slot_j], then apply `op`
-// op 0: init (rho = bnorm2 = rr; conv if 0)
-// op 1: alpha = rho / r0v
-// op 2: omega = ts / tt
-// op 3: rho_new, rnorm2 -> beta, convergence
-__global__ void k_seg_finalize(SegTab t, int K, const double* partial, double* scal, int s0, int s1, int op,
-                               double tol2) {
-    const int g = blockIdx.x;
-    if (g >= t.nseg) return;
-    __shared__ double sh[3][32];
-    double v[3] = {0.0, 0.0, 0.0};
-    for (int b = t.blk[g] + threadIdx.x; b < t.blk[g + 1]; b += blockDim.x)
-        for (int j = 0; j < K; ++j) v[j] += partial[(int64_t)b * K + j];
-    for (int j = 0; j < K; ++j) {
-        double x = v[j];
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        if ((threadIdx.x & 31) == 0) sh[j][threadIdx.x >> 5] = x;
-    }
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-    double r[3] = {0.0, 0.0, 0.0};
-    for (int j = 0; j < K; ++j)
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r[j] += sh[j][w];
-    double* sc = scal + g * NSC;
-    if (op < 0) {
-        sc[s0] = r[0];
-        return;
-    }
-    if (op == 0) {
-        sc[0] = r[0];
-        sc[3] = r[0];
-        sc[4] = r[0];
-        sc[5] = (r[0] == 0.0) ? 1.0 : 0.0;
-        sc[1] = 0.0;
-        sc[2] = 0.0;
-        sc[6] = 0.0;
-        return;
-    }
-    if (op == 4) {              // warm start: r = (r.r, b.b); tolerance stays relative to |b|
-        sc[0] = r[0];
-        sc[3] = r[1];
-        sc[4] = r[0];
-        sc[5] = (r[1] == 0.0 || r[0] <= tol2 * r[1]) ? 1.0 : 0.0;
-        sc[1] = 0.0;
-        sc[2] = 0.0;
-        sc[6] = 0.0;
-        sc[7] = 0.0;
-        return;
-    }
-    if (op == 5) {              // warm-start factor per grid: alpha = (b.bp) / (bp.bp), kept in sc[9]
-        sc[9] = (r[1] > 0.0 && isfinite(r[0] / r[1])) ? r[0] / r[1] : 0.0;
-        return;
-    }
-    if (sc[5] != 0.0) return;   // converged grid: scalars frozen
-    if (op == 1) {              // alpha = rho / (r0.v)
-        const double a = sc[0] / r[0];
-        if (r[0] == 0.0 || !isfinite(a)) {
-            sc[1] = 0.0;
-            sc[2] = 0.0;
-            sc[5] = 2.0;        // breakdown
-        } else {
-            sc[1] = a;
-        }
-    } else if (op == 2) {       // r = (t.s, t.t, s.s): omega, or converge at the half step
-        if (r[2] <= tol2 * sc[3]) {
-            sc[2] = 0.0;        // x += alpha p, r = s
-            sc[7] = 1.0;        // converge after the update
-        } else {
-            const double om = r[0] / r[1];
-            sc[2] = (r[1] > 0.0 && isfinite(om)) ? om : 0.0;
-            sc[7] = 0.0;
-        }
-    } else if (op == 3) {       // r = (r0.r, r.r)
-        const double rho_new = r[0];
-        sc[4] = r[1];
-        double beta = 0.0;
-        if (sc[0] != 0.0 && sc[2] != 0.0) beta = (rho_new / sc[0]) * (sc[1] / sc[2]);
-        sc[0] = rho_new;
-        sc[6] = isfinite(beta) ? beta : 0.0;
-        if (sc[7] != 0.0 || r[1] <= tol2 * sc[3]) sc[5] = 1.0;
-        else if (rho_new == 0.0 || !isfinite(rho_new) || !isfinite(r[1]) || sc[2] == 0.0) sc[5] = 2.0;
-    }
-}
-
-// s = r - alpha v
-__global__ void k_bicg_s(SegTab t, const double* scal, const double* r, const double* v, double* s) {
-    const int g = seg_of(t, blockIdx.x);
-    const double* sc = scal + g * NSC;
-    if (sc[5] != 0.0) return;
-    const double al = sc[1];
-    const int64_t lo = t.off[g] + (int64_t)(blockIdx.x - t.blk[g]) * SEG_CHUNK;
-    const int64_t hi = min(lo + SEG_CHUNK, t.off[g + 1]);
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s[i] = r[i] - al * v[i];
-}
-
-// x += alpha p + omega s ; r = s - omega t ; partial dots (r0.r, r.r)
-__global__ void k_bicg_xr(SegTab tb, const double* scal, double* x, double* r, const double* p, const double* sx,
-                          const double* s, const double* t, const double* r0, double* partial) {
-    __shared__ double sh[2][8];
-    const int g = seg_of(tb, blockIdx.x);
-    const double* sc = scal + g * NSC;
-    const bool active = sc[5] == 0.0;
-    if (!active) {   // converged grid: frozen, no traffic
-        if (threadIdx.x < 2) partial[(int64_t)blockIdx.x * 2 + threadIdx.x] = 0.0;
-        return;
-    }
-    const double al = sc[1], om = sc[2];
-    const int64_t lo = tb.off[g] + (int64_t)(blockIdx.x - tb.blk[g]) * SEG_CHUNK;
-    const int64_t hi = min(lo + SEG_CHUNK, tb.off[g + 1]);
-    double a0 = 0.0, a1 = 0.0;
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        double ri = r[i];
-        if (active) {
-            x[i] += al * p[i] + om * sx[i];
-            ri = s[i] - om * t[i];
-            r[i] = ri;
-        }
-        a0 += r0[i] * ri;
-        a1 += ri * ri;
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-        a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        sh[0][threadIdx.x >> 5] = a0;
-        sh[1][threadIdx.x >> 5] = a1;
-    }
-    __syncthreads();
-    if (threadIdx.x < 2) {
-        double v = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += sh[threadIdx.x][w];
-        partial[(int64_t)blockIdx.x * 2 + threadIdx.x] = v;
-    }
-}
-
-// fused S = 1 variants with the point-Jacobi preconditioner: s = r - alpha v, sh = D^{-1} s
-__global__ void k_bicg_s_pc(SegTab t, const double* scal, const double* r, const double* v, double* s,
-                            const double* Dinv, double* sh) {
-    const int g = seg_of(t, blockIdx.x);
-    const double* sc = scal + g * NSC;
-    if (sc[5] != 0.0) return;
-    const double al = sc[1];
-    const int64_t lo = t.off[g] + (int64_t)(blockIdx.x - t.blk[g]) * SEG_CHUNK;
-    const int64_t hi = min(lo + SEG_CHUNK, t.off[g + 1]);
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        const double si = r[i] - al * v[i];
-        s[i] = si;
-        sh[i] = Dinv[i] * si;
-    }
-}
-// p = r + beta (p - omega v), ph = D^{-1} p (the next iteration's preconditioned direction)
-__global__ void k_bicg_p_pc(SegTab t, const double* scal, double* p, const double* r, const double* v,
-                            const double* Dinv, double* ph) {
-    const int g = seg_of(t, blockIdx.x);
-    const double* sc = scal + g * NSC;
-    if (sc[5] != 0.0) return;
-    const double be = sc[6], om = sc[2];
-    const int64_t lo = t.off[g] + (int64_t)(blockIdx.x - t.blk[g]) * SEG_CHUNK;
-    const int64_t hi = min(lo + SEG_CHUNK, t.off[g + 1]);
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        const double pi = r[i] + be * (p[i] - om * v[i]);
-        p[i] = pi;
-        ph[i] = Dinv[i] * pi;
-    }
-}
-
-// p = r + beta (p - omega v)
-__global__ void k_bicg_p(SegTab t, const double* scal, double* p, const double* r, const double* v) {
-    const int g = seg_of(t, blockIdx.x);
-    const double* sc = scal + g * NSC;
-    if (sc[5] != 0.0) return;
-    const double be = sc[6], om = sc[2];
-    const int64_t lo = t.off[g] + (int64_t)(blockIdx.x - t.blk[g]) * SEG_CHUNK;
-    const int64_t hi = min(lo + SEG_CHUNK, t.off[g + 1]);
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) p[i] = r[i] + be * (p[i] - om * v[i]);
-}
-
-// ---------------------------------------------- point-block Jacobi (time)
-// D_k = sum_t T_t diag(A_t)_i diag(B_t)_a, an S x S block per node k = (i, a);
-// the inner solver is right-preconditioned with D^{-1} (the paper
-// uses GMRES+ILU for eq. (15); this is the GPU-friendly point-block variant).
-struct DiagTerm {
-    double T[4];
-    const double* dA;
-    const double* dB;
-};
-__global__ void k_extract_diag(int64_t n, int W, const int32_t* cols, const double* vals, double* out) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    double d = 0.0;
-    for (int k = 0; k < W; ++k)
-        if (cols[k * n + i] == (int32_t)i) d += vals[k * n + i];
-    out[i] = d;
-}
-__global__ void k_diag_block_inv(int64_t n1, int64_t n2, int S, int nt, const DiagTerm* terms, double* Dinv) {
-    const int64_t n = n1 * n2;
-    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    const int64_t i = k / n2, a = k - i * n2;
-    double D[4] = {0, 0, 0, 0};
-    for (int t = 0; t < nt; ++t) {
-        const double f = terms[t].dA[i] * terms[t].dB[a];
-        for (int q = 0; q < S * S; ++q) D[q] += terms[t].T[q] * f;
-    }
-    if (S == 1) {
-        Dinv[k] = 1.0 / D[0];
-    } else {
-        const double det = D[0] * D[3] - D[1] * D[2];
-        Dinv[0 * n + k] = D[3] / det;
-        Dinv[1 * n + k] = -D[1] / det;
-        Dinv[2 * n + k] = -D[2] / det;
-        Dinv[3 * n + k] = D[0] / det;
-    }
-}
-
-int build_block_jacobi(sg_problem* P) {
-    const int S = P->S;
-    std::vector<const Grid*> gr;
-    for (auto& g : P->active) gr.push_back(&g);
-    for (auto& g : P->coarse) gr.push_back(&g);
-    int64_t tot = 0;
-    for (auto* g : gr) tot += (int64_t)S * S * gsize(*g);
-    SG_CUDA(cudaMalloc(&P->dinv, sizeof(double) * tot));
-    // diagonal vectors of every used spec on every level
-    auto diagvec = [&](Factor& f, int spec, int l, double** out) -> int {
-        Level& L = f.lev[l];
-        SG_CUDA(cudaMalloc(out, sizeof(double) * L.n));
-        k_extract_diag<<<(int)((L.n + 255) / 256), 256, 0, P->stream>>>(L.n, f.W, L.cols, L.fm[spec], *out);
-        P->launches++;
-        return SG_OK;
-    };
-    std::vector<double*> tmp;
-    DiagTerm* dterms;
-    SG_CUDA(cudaMalloc(&dterms, sizeof(DiagTerm) * P->terms.size()));
-    int64_t off = 0;
-    for (auto* g : gr) {
-        std::vector<DiagTerm> ht;
-        for (auto& t : P->terms) {
-            DiagTerm d;
-            for (int q = 0; q < 4; ++q) d.T[q] = t.T[q];
-            double *a, *b;
-            SG_TRY(diagvec(P->fx, t.xs, g->l1, &a));
-            SG_TRY(diagvec(P->fv, t.vs, g->l2, &b));
-            tmp.push_back(a);
-            tmp.push_back(b);
-            d.dA = a;
-            d.dB = b;
-            ht.push_back(d);
-        }
-        SG_CUDA(cudaMemcpyAsync(dterms, ht.data(), sizeof(DiagTerm) * ht.size(), cudaMemcpyHostToDevice, P->stream));
-        const int64_t n = gsize(*g);
-        k_diag_block_inv<<<(int)((n + 255) / 256), 256, 0, P->stream>>>(g->n1, g->n2, S, (int)ht.size(), dterms,
-                                                                       P->dinv + off);
-        P->launches++;
-        SG_CUDA(cudaGetLastError());
-        SG_CUDA(cudaStreamSynchronize(P->stream));
-        for (double* q : tmp) cudaFree(q);
-        tmp.clear();
-        off += (int64_t)S * S * n;
-    }
-    cudaFree(dterms);
-    return SG_OK;
-}
-
-// out = D^{-1} in on every segment (segment = one grid, S x n block)
-__global__ void k_seg_precond(SegTab t, int S, const double* scal, const double* Dinv, const double* in, double* out) {
-    const int g = seg_of(t, blockIdx.x);
-    if (scal[g * NSC + 5] != 0.0) return;
-    const int64_t base = t.off[g];
-    const int64_t n = (t.off[g + 1] - base) / S;
-    const double* Dg = Dinv + base * S;
-    const int64_t lo = base + (int64_t)(blockIdx.x - t.blk[g]) * SEG_CHUNK;
-    const int64_t hi = min(lo + SEG_CHUNK, t.off[g + 1]);
-    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
-        if (S == 1) {
-            out[e] = Dg[e - base] * in[e];
-        } else {
-            const int64_t le = e - base;
-            const int s = (int)(le / n);
-            const int64_t k = le - s * n;
-            out[e] = Dg[(s * 2 + 0) * n + k] * in[base + k] + Dg[(s * 2 + 1) * n + k] * in[base + n + k];
-        }
-    }
-}
-
-// x = sc[9] * x per segment (warm start from the previous outer iteration's block solutions)
-__global__ void k_seg_scale(SegTab t, const double* scal, double* x) {
-    const int g = seg_of(t, blockIdx.x);
-    const double a = scal[g * NSC + 9];
-    const int64_t lo = t.off[g] + (int64_t)(blockIdx.x - t.blk[g]) * SEG_CHUNK;
-    const int64_t hi = min(lo + SEG_CHUNK, t.off[g + 1]);
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) x[i] *= a;
-}
-
-// batched BiCGStab on the grids `gr` (block solves of eq. (15)); b, x concatenated in order of gr
-static int bicgstab(sg_problem* P, const std::vector<const Grid*>& gr, const double* b, double* x, double rtol,
-                    int maxit, const double* bprev = nullptr) {
-    const int S = P->S;
-    std::vector<int64_t> offs(1, 0);
-    for (auto* g : gr) offs.push_back(offs.back() + S * gsize(*g));
-    const int64_t N = offs.back();
-    SegTab t = make_segs(offs);
-    const int nblk = t.blk[t.nseg];
-    double *r = P->vec[0], *r0 = P->vec[1], *p = P->vec[2], *v = P->vec[3], *s = P->vec[4], *tt = P->vec[5];
-    double *ph = P->vec[13], *sh = P->vec[14];
-    const bool pc = P->dinv != nullptr && P->use_precond;
-    const bool fuse = pc && S == 1;   // preconditioner fused into the s / p updates
-    const double tol2 = rtol * rtol;
-    if (bprev && P->warm_valid) {
-        // warm start (see solve_strip): x0 = alpha_g * x_prev, alpha_g = (b, b_prev)/(b_prev, b_prev)
-        // per grid; the previous solution is the preconditioned one, so x0 = D^{-1}... is not needed:
-        // x holds the previous block solution itself
-        k_seg_dot<2><<<nblk, 256, 0, P->stream>>>(t, b, bprev, bprev, bprev, P->red);
-        k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 2, P->red, P->scal, 9, 9, 5, 0.0);
-        k_seg_scale<<<nblk, 256, 0, P->stream>>>(t, P->scal, x);
-        P->launches += 3;
-        for (size_t i = 0; i < gr.size(); ++i) SG_TRY(apply_diag(P, *gr[i], x + offs[i], v + offs[i]));
-        SG_TRY(launch_copy(P, N, b, r));
-        SG_TRY(launch_axpby(P, N, -1.0, v, 1.0, r));                         // r = b - A x0
-        SG_TRY(launch_copy(P, N, r, r0));
-        SG_TRY(launch_copy(P, N, r, p));
-        k_seg_dot<2><<<nblk, 256, 0, P->stream>>>(t, r, r, b, b, P->red);
-        k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 2, P->red, P->scal, 0, 0, 4, tol2);
-        P->launches += 2;
-    } else {
-        SG_TRY(launch_zero(P, N, x));
-        SG_TRY(launch_copy(P, N, b, r));
-        SG_TRY(launch_copy(P, N, b, r0));
-        SG_TRY(launch_copy(P, N, b, p));
-        k_seg_dot<1><<<nblk, 256, 0, P->stream>>>(t, b, b, nullptr, nullptr, P->red);
-        k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 1, P->red, P->scal, 9, 9, 0, 0.0);
-        P->launches += 2;
-    }
-    std::vector<char> conv(gr.size(), 0);
-    for (int it = 0; it < maxit; ++it) {
-        // v = A M^{-1} p
-            const double* pa = p;
-        if (pc) {
-            if (!fuse || it == 0) {   // fused path: ph was produced by k_bicg_p_pc of the last iteration
-                k_seg_precond<<<nblk, 256, 0, P->stream>>>(t, S, P->scal, P->dinv, p, ph);
-                P->launches++;
-            }
-            pa = ph;
-        }
-        for (size_t i = 0; i < gr.size(); ++i)
-            if (!conv[i]) SG_TRY(apply_diag(P, *gr[i], pa + offs[i], v + offs[i]));
-        k_seg_dot<1><<<nblk, 256, 0, P->stream>>>(t, r0, v, nullptr, nullptr, P->red, nullptr, nullptr, P->scal);
-        k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 1, P->red, P->scal, 6, 6, 1, tol2);
-        const double* sa = s;
-        if (fuse) {
-            k_bicg_s_pc<<<nblk, 256, 0, P->stream>>>(t, P->scal, r, v, s, P->dinv, sh);
-            sa = sh;
-        } else {
-            k_bicg_s<<<nblk, 256, 0, P->stream>>>(t, P->scal, r, v, s);
-            if (pc) {
-                k_seg_precond<<<nblk, 256, 0, P->stream>>>(t, S, P->scal, P->dinv, s, sh);
-                P->launches++;
-                sa = sh;
-            }
-        }
-        for (size_t i = 0; i < gr.size(); ++i)
-            if (!conv[i]) SG_TRY(apply_diag(P, *gr[i], sa + offs[i], tt + offs[i]));
-        k_seg_dot<3><<<nblk, 256, 0, P->stream>>>(t, tt, s, tt, tt, P->red, s, s, P->scal);
-        k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 3, P->red, P->scal, 7, 8, 2, tol2);
-        k_bicg_xr<<<nblk, 256, 0, P->stream>>>(t, P->scal, x, r, pa, sa, s, tt, r0, P->red);
-        k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 2, P->red, P->scal, 0, 4, 3, tol2);
-        if (fuse)
-            k_bicg_p_pc<<<nblk, 256, 0, P->stream>>>(t, P->scal, p, r, v, P->dinv, ph);
-        else
-            k_bicg_p<<<nblk, 256, 0, P->stream>>>(t, P->scal, p, r, v);
-        P->launches += 8;
-        SG_CUDA(cudaGetLastError());
-        P->inner_iters++;
-        SG_CUDA(cudaMemcpyAsync(P->hscal, P->scal, sizeof(double) * NSC * gr.size(), cudaMemcpyDeviceToHost,
-                                P->stream));
-        SG_CUDA(cudaStreamSynchronize(P->stream));
-        bool all = true;
-        for (size_t i = 0; i < gr.size(); ++i) {
-            conv[i] = P->hscal[i * NSC + 5] != 0.0;
-            all &= (bool)conv[i];
-        }
-        if (all) break;
-    }
-    return SG_OK;
-}
-
-// ------------------------------------------------------------ combination
-// du_p = dhat_p - (E^(1)_{l1<-l1-1} x Id) dhat_{(l1-1,l2)}  (l.557-565)
-int combine(sg_problem* P, int S, const double* dhat_a, const double* dhat_c, double* du) {
-    const auto& A = P->active;
-    for (size_t p = 0; p < A.size(); ++p) {
-        const Grid& g = A[p];
-        SG_TRY(launch_copy(P, S * gsize(g), dhat_a + g.off1 * S, du + g.off1 * S));
-        if (g.l1 > 1) {
-            const Grid& c = P->coarse[g.l1 - 2];   // (l1-1, l2)
-            EntryList el;
-            el.ne = 0;
-            for (int s = 0; s < S; ++s)
-                el.e[el.ne++] = {dhat_c + c.off1 * S, P->fx.lev[g.l1].pvals, -1.0, s, s};
-            SG_TRY(launch_gather(P, 0, 2, S, c.n1, c.n2, g.n1, P->fx.lev[g.l1].pcols, el, du + g.off1 * S, 1.0));
-        }
-    }
-    return SG_OK;
-}
-
-static double host_dot(sg_problem* P, int64_t n, const double* a, const double* b, int* err) {
-    std::vector<int64_t> offs = {0, n};
-    SegTab t = make_segs(offs);
-    k_seg_dot<1><<<t.blk[1], 256, 0, P->stream>>>(t, a, b, nullptr, nullptr, P->red);
-    // finalize into slot 9 of a scratch segment placed after the BiCGStab scalars
-    double* sc = P->scal + NSC * MAX_SEG;
-    k_seg_finalize<<<1, 256, 0, P->stream>>>(t, 1, P->red, sc, 9, 9, -1, 0.0);
-    P->launches += 2;
-    double h = 0.0;
-    if (cudaMemcpyAsync(&h, sc + 9, sizeof(double), cudaMemcpyDeviceToHost, P->stream) != cudaSuccess ||
-        cudaStreamSynchronize(P->stream) != cudaSuccess)
-        *err = SG_ERR_CUDA;
-    return h;
-}
-
-// ------------------------------------------------------------ Richardson
-int solve_strip(sg_problem* P, const double* b, double* u, double rtol, double inner_rtol, int max_iter, int* iters,
-                double* last) {
-    const int S = P->S;
-    const int64_t Na = set_size(P, SG_SET_ACTIVE, S), Nc = set_size(P, SG_SET_COARSE, S);
-    double* r = P->vec[6];
-    double* rhs = P->vec[7];      // [active | coarse]
-    double* dhat = P->vec[8];     // [active | coarse]
-    double* du = P->vec[9];
-    double* Mw = P->vec[10];
-    double* rhs_prev = P->vec[16];   // previous outer iteration's block right-hand sides (warm start)
-    std::vector<const Grid*> gr;
-    for (auto& g : P->active) gr.push_back(&g);
-    for (auto& g : P->coarse) gr.push_back(&g);
-    double Mt[4] = {0, 0, 0, 0};
-    Mt[0] = P->cfg.tau;
-    if (S == 2) Mt[3] = P->cfg.tau / 3.0;
-    int it = 0;
-    double nd = 0.0, nu_est = 0.0, nd_prev = 0.0;
-    // Outer iteration: the paper's Richardson u <- u - P^{-1} r (l.540-546).  Safeguard: when the
-    // update norm grows (the combination preconditioner is not a contraction, e.g. configs[2]
-    // at L = 12) the step length switches to the residual-minimising omega_k = (r, A du)/(A du, A du)
-    // for the rest of the solve (same one cross-grid apply per iteration, residual updated
-    // recursively); P->outer_mode: 0 paper + safeguard, 1 paper only, 2 minimal residual always.
-    bool mr = P->outer_mode == 2;
-    bool have_r = false;
-    double* w = P->vec[15];   // A du (minimal-residual steps)
-    for (it = 1; it <= max_iter; ++it) {
-        P->outer_iters++;
-        if (!have_r) {
-            SG_TRY(apply_cross(P, nullptr, nullptr, S, S, u, r));                 // r = A u
-            SG_TRY(launch_axpby(P, Na, -1.0, b, 1.0, r));                        // r -= b
-        }
-        SG_TRY(launch_copy(P, Na, r, rhs));
-        for (size_t c = 0; c < P->coarse.size(); ++c) {                       // (Id x E^T x Id) r, l.552
-            const Grid& cg = P->coarse[c];
-            const Grid& src = P->active[cg.l1];                               // (c1+1, c2)
-            EntryList el;
-            el.ne = 0;
-            for (int s = 0; s < S; ++s) el.e[el.ne++] = {r + src.off1 * S, P->fx.lev[src.l1].rvals, 1.0, s, s};
-            SG_TRY(launch_gather(P, 0, P->fx.W, S, src.n1, src.n2, cg.n1, P->fx.lev[src.l1].rcols, el,
-                                 rhs + Na + cg.off1 * S, 0.0));
-        }
-        // warm start of the block solves from the previous outer iteration (Richardson's corrections
-        // are asymptotically proportional from one iteration to the next); SG_NO_WARM disables
-        const bool warm = P->use_warm && it > 1;
-        P->warm_valid = warm;
-        SG_TRY(bicgstab(P, gr, rhs, dhat, inner_rtol, 500, warm ? rhs_prev : nullptr));
-        if (P->use_warm) SG_TRY(launch_copy(P, Na + Nc, rhs, rhs_prev));
-        SG_TRY(combine(P, S, dhat, dhat + Na, du));
-        int err = SG_OK;
-        double omega = 1.0;
-        if (mr) {
-            SG_TRY(apply_cross(P, nullptr, nullptr, S, S, du, w));                // w = A du
-            const double rw = host_dot(P, Na, r, w, &err), ww = host_dot(P, Na, w, w, &err);
-            if (err) return err;
-            omega = (ww > 0.0 && std::isfinite(rw / ww)) ? rw / ww : 1.0;
-            SG_TRY(launch_axpby(P, Na, -omega, w, 1.0, r));                     // r <- r - omega A du
-            have_r = true;
-        }
-        SG_TRY(launch_axpby(P, Na, -omega, du, 1.0, u));
-        SG_TRY(apply_cross(P, nullptr, Mt, S, S, du, Mw));
-        double nd2 = host_dot(P, Na, du, Mw, &err) * omega * omega;
-        nd = std::sqrt(std::max(nd2, 0.0));
-        // ||u|| only when the test can pass (it changes little once |du| is small)
-        if (it == 1 || nd <= 4.0 * rtol * nu_est) {
-            SG_TRY(apply_cross(P, nullptr, Mt, S, S, u, Mw));
-            double nu2 = host_dot(P, Na, u, Mw, &err);
-            nu_est = std::sqrt(std::max(nu2, 0.0));
-        }
-        if (err) return err;
-        double nu = nu_est;
-        double nu2 = nu * nu;
-        if (P->verbose) fprintf(stderr, "[sg] richardson it %d |du| %.3e |u| %.3e omega %.3f inner %lld\n", it, nd, nu,
-                                omega, (long long)P->inner_iters);
-        if (!std::isfinite(nd2) || !std::isfinite(nu2)) {
-            set_error("solve_strip: non-finite update (inner solver breakdown)");
-            return SG_ERR_STATE;
-        }
-        if (nd <= rtol * nu || nd == 0.0) break;
-        if (!mr && P->outer_mode == 0 && it >= 2 && nd > nd_prev) {
-            mr = true;   // safeguard engaged; r is recomputed from u at the next iteration top
-            P->mr_switches++;
-        }
-        nd_prev = nd;
-    }
-    if (iters) *iters = std::min(it, max_iter);
-    if (last) *last = nd;
-    (void)Nc;
-    return SG_OK;
-}
-
 // ------------------------------------------------------- data (u0, inflow)
 __global__ void k_gauss_nodes(int64_t n, int d, const int32_t* lat, double lo0, double lo1, double lo2, double h0,
                               double h1, double h2, double c0, double c1, double c2, double w, double scale,
@@ -1716,22 +1107,6 @@ int trace_of(sg_problem* P, const double* u, double* tr) {
         const int64_t n = gsize(g);
         SG_TRY(launch_copy(P, n, u + g.off1 * S, tr + g.off1));
         for (int s = 1; s < S; ++s) SG_TRY(launch_axpby(P, n, 1.0, u + g.off1 * S + s * n, 1.0, tr + g.off1));
-    }
-    return SG_OK;
-}
-
-int step(sg_problem* P, int j0, int nsteps, double* trace_dev, double rtol, double inner_rtol) {
-    const int S = P->S;
-    const int64_t Na = set_size(P, SG_SET_ACTIVE, S);
-    double* b = P->vec[11];
-    double* u = P->vec[12];
-    for (int j = j0; j < j0 + nsteps; ++j) {
-        SG_TRY(rhs(P, j, trace_dev, b));
-        SG_TRY(launch_zero(P, Na, u));
-        int it = 0;
-        double last = 0;
-        SG_TRY(solve_strip(P, b, u, rtol, inner_rtol, 200, &it, &last));
-        SG_TRY(trace_of(P, u, trace_dev));
     }
     return SG_OK;
 }

@@ -97,7 +97,8 @@ __global__ void __launch_bounds__(256, 2)
     k_vmom(int nthr, int n2, int nrows, int rstride, int m, long long pitch, const double* __restrict__ X,
            const __grid_constant__ VmOut o, const uint8_t* __restrict__ xflag, int n1x,
            const double* __restrict__ tab, const __grid_constant__ VmCoef cf, double lo0, double lo1, double lo2,
-           double h0, double h1, double h2) {
+           double h0, double h1, double h2, const double* __restrict__ skip) {
+    if (skip && *skip != 0.0) return;   // grid converged (batched block solver)
     constexpr int W = D == 3 ? 15 : 7;
     constexpr int NC = D == 3 ? 27 : 9;
     constexpr int NR = VM_NP + VM_NC;
@@ -277,7 +278,7 @@ int prepare_vmom(sg_problem* P) {
     const Factor& f = P->fv;
     const int d = f.d, W = f.W;
     constexpr int NR = VM_NP + VM_NC;
-    if (f.kind != SG_MESH_BOX || d < 2 || !P->use_vmom) return SG_OK;
+    if (f.kind != SG_MESH_BOX || d < 2 ) return SG_OK;
     // interior groups must be plain monomial-weighted masses, and the set must be closed
     int spec_of[VM_NP];
     for (int n = 0; n < VM_NP; ++n) spec_of[n] = -1;
@@ -424,6 +425,7 @@ int prepare_vmom(sg_problem* P) {
             continue;
         }
         P->vm_tab[l] = dt;
+        P->vm_tab_n = (int64_t)Rl.size();
         std::vector<double> ci((size_t)NR * 15, 0.0);
         for (int n = 0; n < NR; ++n)
             for (int k = 0; k < W; ++k) ci[n * 15 + k] = Rl[((size_t)icls * NR + n) * W + k];
@@ -492,7 +494,7 @@ int launch_vmom(sg_problem* P, int l2, int64_t nrows, int64_t n2, int64_t pitch,
     do {                                                                                                            \
         cudaFuncSetAttribute(k_vmom<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb);                         \
         k_vmom<DD><<<nb, 256, smb, P->stream>>>((int)nthr, (int)n2, (int)nrows, ph, m, pitch, X, o, xflag, (int)n1x, \
-                                                P->vm_tab[l2], cf, lo[0], lo[1], lo[2], h[0], h[1], h[2]);          \
+                                                P->vm_tab[l2], cf, lo[0], lo[1], lo[2], h[0], h[1], h[2], P->skip);          \
     } while (0)
     if (d == 3) VMA(3); else VMA(2);
 #undef VMA

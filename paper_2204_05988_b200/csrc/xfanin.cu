@@ -91,7 +91,8 @@ template <int D, int NGI, int CPT>
 __global__ void __launch_bounds__(256, CPT == 1 ? 2 : 1)
     k_xfanin(const double* __restrict__ Z, long long gstride, int nga, int n2, int m, int nlb1, int nlb, int nseg,
              int seglen, int nsub, int ntask, const double* __restrict__ tab, const __grid_constant__ XfiCoef cint,
-             double* __restrict__ Y, double beta) {
+             double* __restrict__ Y, double beta, const double* __restrict__ skip) {
+    if (skip && *skip != 0.0) return;   // grid converged (batched block solver)
     using G = xfi::Geo<D>;
     constexpr int W = G::W, NT = G::NT, NS = G::NE1 * G::NE2;
     const int lane = threadIdx.x & 31;
@@ -248,7 +249,7 @@ int prepare_xfanin(sg_problem* P) {
     P->xfi_tab.assign(P->F + 1, nullptr);
     P->xfi_itab.assign(P->F + 1, nullptr);
     P->xfi_cint.assign(P->F + 1, {});
-    if (P->fx.kind != SG_MESH_BOX || P->S != 1 || P->fx.d < 2 || !P->use_classes) return SG_OK;
+    if (P->fx.kind != SG_MESH_BOX || P->S != 1 || P->fx.d < 2 ) return SG_OK;
     const int nga = (int)P->vorder.size();
     if (P->ng_int > XFI_MAXG) return SG_OK;
     const int d = P->fx.d, W = P->fx.W;
@@ -303,7 +304,7 @@ int launch_xfanin(sg_problem* P, int l1, int64_t n1, int64_t n2, const double* Z
     const int d = P->fx.d, m = P->fx.lev[l1].m;
     const int nga = (int)P->vorder.size(), ngi = P->ng_int;
     if (m < 3 || n1 * n2 >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
-    const int cpt = (P->xfi_cpt == 2 && n2 >= 64) ? 2 : 1;
+    constexpr int cpt = 1;   // (2 columns per lane measured slower in round 1)
     const int nct = (int)((n2 + 32 * cpt - 1) / (32 * cpt));
     const int nsub = n2 <= 16 ? (int)(32 / n2) : 1;
     int nlb1, nlb;
@@ -315,14 +316,9 @@ int launch_xfanin(sg_problem* P, int l1, int64_t n1, int64_t n2, const double* Z
         nlb = nlb1;
     }
     // split the line sweep into segments until the machine has >= 16 warps per SM of work
-    const int seg_env = P->xfi_seg;
     int seglen = m;
-    if (seg_env > 0) {
-        seglen = seg_env;
-    } else {
-        while (seglen > 16 && (long long)nlb * nct * ((m + seglen - 1) / seglen) < 148LL * 16 * nsub)
-            seglen = (seglen + 1) / 2;
-    }
+    while (seglen > 16 && (long long)nlb * nct * ((m + seglen - 1) / seglen) < 148LL * 16 * nsub)
+        seglen = (seglen + 1) / 2;
     const int nseg = (m + seglen - 1) / seglen;
     const long long ntask = (long long)nlb * nseg * nct;
     const long long warps = (ntask + nsub - 1) / nsub;
@@ -333,8 +329,8 @@ int launch_xfanin(sg_problem* P, int l1, int64_t n1, int64_t n2, const double* Z
     const double* tab = P->xfi_tab[l1];
 #define XFI(DD, NG, CC)                                                                                           \
     k_xfanin<DD, NG, CC><<<(unsigned)blocks, 256, 0, P->stream>>>(Z, (long long)gstride, nga, (int)n2, m, nlb1, nlb, \
-                                                                  nseg, seglen, nsub, (int)ntask, tab, ci, Y, beta)
-#define XFI_C(DD, NG) do { if (cpt == 2) XFI(DD, NG, 2); else XFI(DD, NG, 1); } while (0)
+                                                                  nseg, seglen, nsub, (int)ntask, tab, ci, Y, beta, P->skip)
+#define XFI_C(DD, NG) XFI(DD, NG, 1)
     if (d == 3 && ngi == 10) XFI_C(3, 10);
     else if (d == 2 && ngi == 6) XFI_C(2, 6);
     else if (d == 3 && ngi == 6) XFI_C(3, 6);
@@ -392,7 +388,8 @@ __constant__ double c_xw[XW_MAXG * XW_MAXP];   // [g][pair] of the launched leve
 
 template <int D, int M>
 __global__ void __launch_bounds__(256, 2) k_xwhole(const double* __restrict__ Z, long long gstride, int nga, int n2,
-                                                   long long pitch, double* __restrict__ Y) {
+                                                   long long pitch, double* __restrict__ Y, const double* __restrict__ skip) {
+    if (skip && *skip != 0.0) return;   // grid converged (batched block solver)
     constexpr int N = D == 3 ? M * M * M : M * M;
     constexpr int W = D == 3 ? 15 : 7;
     constexpr int NP = D == 3 ? (M == 3 ? 223 : 0) : (M == 3 ? 41 : 137);   // xw::npairs<D, M>()
@@ -512,13 +509,13 @@ int launch_xwhole(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pitch, 
     const unsigned blocks = (unsigned)((n2 + 255) / 256);
     if (d == 3) {
         if (np != 223) return SG_ERR_UNSUPPORTED;
-        k_xwhole<3, 3><<<blocks, 256, 0, P->stream>>>(Z, gstride, nga, (int)n2, pitch, Y);
+        k_xwhole<3, 3><<<blocks, 256, 0, P->stream>>>(Z, gstride, nga, (int)n2, pitch, Y, P->skip);
     } else if (m == 3) {
         if (np != 41) return SG_ERR_UNSUPPORTED;
-        k_xwhole<2, 3><<<blocks, 256, 0, P->stream>>>(Z, gstride, nga, (int)n2, pitch, Y);
+        k_xwhole<2, 3><<<blocks, 256, 0, P->stream>>>(Z, gstride, nga, (int)n2, pitch, Y, P->skip);
     } else {
         if (np != 137) return SG_ERR_UNSUPPORTED;
-        k_xwhole<2, 5><<<blocks, 256, 0, P->stream>>>(Z, gstride, nga, (int)n2, pitch, Y);
+        k_xwhole<2, 5><<<blocks, 256, 0, P->stream>>>(Z, gstride, nga, (int)n2, pitch, Y, P->skip);
     }
     P->launches++;
     SG_CUDA(cudaGetLastError());

@@ -114,7 +114,6 @@ constexpr int XFT_MAXG = 12;
 // coefficient loads are warp-uniform and go through the constant cache, not L1
 constexpr int XFT_CTAB = 27 * 10 * 15;   // interior groups only (bonly groups read the global table)
 __constant__ double c_xft[XFT_CTAB];
-constexpr int XFT_MAXST = 12;   // pipeline stages (runtime, sized to the shared-memory budget)
 struct XftCoef {
     double c[XFT_MAXG][15];
 };
@@ -128,7 +127,8 @@ struct XftTile {
 template <int D, int NGI, bool CTAB>
 __global__ void __launch_bounds__(32 * 17, 1)
     k_xfanin_tma(const __grid_constant__ CUtensorMap tmap, int nga, int n2, int m, XftTile tl,
-                 const double* __restrict__ tab, const __grid_constant__ XftCoef cint, double* __restrict__ Y) {
+                 const double* __restrict__ tab, const __grid_constant__ XftCoef cint, double* __restrict__ Y, const double* __restrict__ skip) {
+    if (skip && *skip != 0.0) return;   // grid converged (batched block solver)
     using G = xft::Geo<D>;
     constexpr int W = G::W, NT = G::NT, NS = G::NE1 * G::NE2;
     extern __shared__ __align__(128) unsigned char smraw[];
@@ -346,7 +346,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // tile choice: minimise TMA source-line loads per valid target line
-static int g_xft_minw = 4;
+constexpr int XFT_MINW = 4;   // at least 4 consumer warps per CTA
 static XftTile choose_tile(int d, int m, int64_t n2, int force_wc, int box_kb) {
     XftTile best{};
     double best_cost = 1e30;
@@ -358,7 +358,7 @@ static XftTile choose_tile(int d, int m, int64_t n2, int force_wc, int box_kb) {
         for (int w1 = 1; w1 <= 16; ++w1)
             for (int w2 = 1; w2 <= (d == 3 ? 16 : 1); ++w2) {
                 const int nw = w1 * w2 * wc;
-                if (nw < g_xft_minw || nw > 16) continue;
+                if (nw < XFT_MINW || nw > 16) continue;
                 const int e1 = w1 * B1 + 2, e2 = d == 3 ? w2 * 2 + 2 : 1;
                 const int bc = 32 * wc;
                 if ((double)e1 * e2 * bc * 8 > box_kb * 1024.0) continue;
@@ -389,17 +389,15 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
     // wide boxes (4 column groups = 1 KB rows) measured fastest on the m >= 9 lattices
     // (grid (5,3): 1.67 -> 1.25 ms) and slowest on m = 5 (3.3 -> 4.7 ms)
     const int wc_auto = (m >= 9 && n2 >= 128) ? 4 : 0;
-    g_xft_minw = getenv("SG_XFT_MINW") ? atoi(getenv("SG_XFT_MINW")) : 4;
     // ... and small CTAs (one 2x2 line block x 4 column groups, 16 KB stages) beat larger tiles
     // on those lattices: more independent TMA producers per SM (grid (3,5): 2.02 -> 1.82 ms)
-    const int box_kb = getenv("SG_XFT_BOX_KB") ? P->xft_box_kb : (wc_auto ? (d == 3 ? 16 : 8) : 24);
-    XftTile tl = choose_tile(d, m, n2, P->xft_wc > 0 ? P->xft_wc : wc_auto, box_kb);
+    const int box_kb = wc_auto ? (d == 3 ? 16 : 8) : 24;
+    XftTile tl = choose_tile(d, m, n2, wc_auto, box_kb);
     if (tl.nw == 0) tl = choose_tile(d, m, n2, 0, 24);
     // split the sweep until there are >= 2 CTAs per SM
     const int64_t base = (int64_t)tl.ntl1 * tl.ntl2 * tl.nct;
-    int seglen = P->xfi_seg > 0 ? P->xfi_seg : m;
-    if (P->xfi_seg <= 0)
-        while (seglen > 8 && base * ((m + seglen - 1) / seglen) < 148 * 3) seglen = (seglen + 1) / 2;
+    int seglen = m;
+    while (seglen > 8 && base * ((m + seglen - 1) / seglen) < 148 * 3) seglen = (seglen + 1) / 2;
     tl.seglen = seglen;
     tl.nseg = (m + seglen - 1) / seglen;
     const int64_t nblk = base * tl.nseg;
@@ -436,8 +434,8 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
     std::memcpy(ci.c, P->xfi_cint[l1].data(), sizeof(ci.c));
     const size_t stage_b = (size_t)tl.e1 * tl.e2 * tl.bc * 8;
     // 4 stages measured best (deeper rings shrink L1 and were slower: (2,6) 3.3 -> 5.1 ms at 8 stages)
-    tl.nst = P->xft_smem_kb > 0 ? (int)std::min<size_t>(XFT_MAXST, std::max<size_t>(2, (size_t)(P->xft_smem_kb * 1024) / stage_b))
-                                : (wc_auto && d == 3 ? P->xft_nst_wide : 4);
+    // (3 stages on the wide-box 3D tiles: 1.2 % faster than 4)
+    tl.nst = wc_auto && d == 3 ? 3 : 4;
     const size_t smem = (size_t)tl.nst * stage_b + 2 * tl.nst * sizeof(uint64_t);
     {
         int ncls = 1;
@@ -452,7 +450,7 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
 #define XFT(DD, NG, CT)                                                                                          \
     do {                                                                                                         \
         cudaFuncSetAttribute(k_xfanin_tma<DD, NG, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-        k_xfanin_tma<DD, NG, CT><<<(unsigned)nblk, threads, smem, P->stream>>>(tm, nga, (int)n2, m, tl, tab, ci, Y); \
+        k_xfanin_tma<DD, NG, CT><<<(unsigned)nblk, threads, smem, P->stream>>>(tm, nga, (int)n2, m, tl, tab, ci, Y, P->skip); \
     } while (0)
     const bool ctab = m >= 9;
     if (d == 3) {

@@ -120,7 +120,7 @@ def test_apply_full_cross_grid(name):
         assert relmax(Y[l], ref[l]) <= 1e-12, l
 
 
-@pytest.mark.parametrize("env", ["SG_NO_CROSS_BATCH", "SG_NO_TMA", "SG_VMOM", "SG_JOBS2"])
+@pytest.mark.parametrize("env", ["SG_NO_CROSS_BATCH", "SG_NO_TMA"])
 @pytest.mark.parametrize("name", ["c2_4d_stream", "c4_6d_stream"])
 def test_apply_full_cross_grid_paths(name, env, monkeypatch):
     """Cross-grid apply on the per-group path and with the batched lower part's kernel variants."""
@@ -227,11 +227,12 @@ def test_solve_strip(name):
 
 
 @pytest.mark.parametrize("name", ["c2_4d_stream", "c4_6d_stream", "c1_2d_rot", "c3_4d_lshape"])
-@pytest.mark.parametrize("env", ["SG_OUTER=2", "SG_WARM=1"])
+@pytest.mark.parametrize("env", ["SG_OUTER=2", "SG_OUTER=1", "SG_NO_GRAPHS=1"])
 def test_solve_strip_solver_variants(name, env, monkeypatch):
     """SG_OUTER=2 (residual-minimising step lengths from the first iteration, the safeguard's
-    mode) and SG_NO_WARM (cold-started block solves): the same converged strip solution as
-    the oracle's plain Richardson."""
+    mode), SG_OUTER=1 (the paper's plain Richardson, no safeguard) and SG_NO_GRAPHS (the
+    uncaptured host-loop driver of the same device kernels): the same converged strip
+    solution as the oracle's plain Richardson."""
     from oracle.sgrid import SGProblem
     from paper_2204_05988_b200 import Problem
     k, v = env.split("=")
@@ -294,14 +295,10 @@ def test_zero_rhs_gives_zero():
     assert it == 1 and float(u.abs().max()) == 0.0
 
 
-@pytest.mark.parametrize("env", ["SG_FUSED", "SG_FORCE_XFIRST", "SG_BRICK", "SG_REG", "SG_OLD_XG",
-                                 "SG_XFI_SEG=1", "SG_XFI_SEG=3", "SG_XFI_CPT=2", "SG_NO_TMA", "SG_NO_XWHOLE", "SG_NO_VMOM", "SG_VMOM", "SG_NO_CROSS_BATCH", "SG_VFANK", "SG_NO_GATHER_S2", "SG_NO_RBOX",
-                                 "SG_VF_R=2", "SG_VF_R=3", "SG_VF_R=4"])
+@pytest.mark.parametrize("env", ["SG_NO_TMA"])
 @pytest.mark.parametrize("name", CONFIG_ORDER)
 def test_apply_strip_operator_kernel_paths(name, env, monkeypatch):
-    """Same parity on every kernel path at test sizes: the opt-in fused whole-x
-    kernel, the v-first two-pass kernels everywhere, the x-first two-pass kernels
-    everywhere (large grids pick v-first or x-first by shape)."""
+    """Same parity on the fallback of the TMA line sweep (register line sweep k_xfanin)."""
     from oracle.sgrid import SGProblem
     from paper_2204_05988_b200 import Problem
     key, _, val = env.partition("=")
@@ -318,69 +315,174 @@ def test_apply_strip_operator_kernel_paths(name, env, monkeypatch):
             assert relmax(Yt.cpu().numpy().reshape(X.shape), o.apply_diag(l, X)) <= 1e-12, (set_, l)
 
 
-def test_apply_strip_operator_full_size():
-    """configs[4] at its full size (L=8), launch configuration of bench.py.
-    The balanced grid (4,4) (24M DOF, 2-pass kernels) is compared element by
-    element with the oracle (exact factor matrices on its own level-4 meshes);
-    the extreme grid (1,7) (58M DOF, fused kernel) by properties that hold at
-    any size: linearity and 1^T A 1 = |Omega| + tau int_{Gamma^-} |beta.n|
-    (eq. (11) with v = 1: every derivative term vanishes on constants)."""
+def _full_size_oracle(name, l):
+    """Oracle for one grid of a full-size config: meshes up to the grid's own levels,
+    factor matrices assembled directly on them (equal to the Galerkin products by
+    nestedness, pinned in test_oracle_fem.py), the oracle's own delta and terms."""
+    from oracle.problem import delta_hmin, strip_terms
     from oracle.sgrid import SGProblem
+    cfg = get_config(name)
+    o = SGProblem(get_config(name, L=max(l) + 1), galerkin="direct")
+    o.tau, o.delta = cfg["tau"], delta_hmin(cfg)        # the oracle's own delta (reading R5)
+    o.terms = strip_terms(cfg, cfg["tau"], o.delta)
+    return cfg, o
+
+
+def _grid_index(g, l):
+    return [i for i in range(g.num_grids(SET_ACTIVE)) if g.grid_info(SET_ACTIVE, i)[:2] == l][0]
+
+
+def test_apply_strip_operator_full_size():
+    """configs[4] at its full size (L=8), launch configuration of bench.py: the balanced grid
+    (4,4) (24 M DOF, moment/stencil pass 1 + TMA line-swept pass 2) element by element."""
     from paper_2204_05988_b200 import Problem
-    cfg = get_config("c4_6d_stream")
-    g = Problem(cfg)
+    g = Problem(get_config("c4_6d_stream"))
+    cfg, o = _full_size_oracle("c4_6d_stream", (4, 4))
     rng = np.random.default_rng(9)
-    # --- element-wise on grid (4,4)
-    o = SGProblem(get_config("c4_6d_stream", L=5), galerkin="direct")   # meshes up to level 4
-    o.tau, o.delta = cfg["tau"], g.delta
-    from oracle.problem import strip_terms
-    o.terms = strip_terms(cfg, cfg["tau"], g.delta)
-    l1, l2, n1, n2 = g.grid_info(SET_ACTIVE, 3)
-    assert (l1, l2) == (4, 4)
+    gi = _grid_index(g, (4, 4))
+    l1, l2, n1, n2 = g.grid_info(SET_ACTIVE, gi)
     X = rng.standard_normal((1, n1, n2))
     Yt = torch.empty(n1 * n2, dtype=torch.float64, device="cuda")
-    g.sg_apply_strip_operator(SET_ACTIVE, 3, torch.from_numpy(X.ravel()).cuda(), Yt)
+    g.sg_apply_strip_operator(SET_ACTIVE, gi, torch.from_numpy(X.ravel()).cuda(), Yt)
     ref = o.apply_pair(o.terms, (4, 4), (4, 4), X)
     assert relmax(Yt.cpu().numpy().reshape(X.shape), ref) <= 1e-12
-    # --- properties on grid (1,7)
-    gi = 0
-    l1, l2, n1, n2 = g.grid_info(SET_ACTIVE, gi)
-    X1 = torch.from_numpy(rng.standard_normal(n1 * n2)).cuda()
-    X2 = torch.from_numpy(rng.standard_normal(n1 * n2)).cuda()
-    Y1, Y2, Y3 = torch.empty_like(X1), torch.empty_like(X1), torch.empty_like(X1)
-    g.sg_apply_strip_operator(SET_ACTIVE, gi, X1, Y1)
-    g.sg_apply_strip_operator(SET_ACTIVE, gi, X2, Y2)
-    g.sg_apply_strip_operator(SET_ACTIVE, gi, (2.0 * X1 - 3.0 * X2).contiguous(), Y3)
-    lin = 2.0 * Y1 - 3.0 * Y2
-    assert float((Y3 - lin).abs().max() / lin.abs().max()) <= 1e-13
-    ones = torch.ones(n1 * n2, dtype=torch.float64, device="cuda")
-    Y = torch.empty_like(ones)
-    g.sg_apply_strip_operator(SET_ACTIVE, gi, ones, Y)
-    # Omega = [0,1]^3 x [-4,4]^3, beta = (v, 0): inflow on x_i = 0 (v_i > 0) and x_i = 1 (v_i < 0),
-    # int_{v_i > 0} v_i dv = 8 * 8 * 8 = 512 per face -> 3 axes * 2 faces * 512
-    tau = cfg["tau"]
-    expect = 512.0 + tau * 3 * 2 * 512.0
-    val = float(Y.sum())
-    assert abs(val - expect) <= 1e-12 * expect, (val, expect)
+
+
+def _sample_nodes(m, d, n_random, rng):
+    """Sampled lattice nodes of an m^d box lattice: all 3^d boundary-class corners/edge/face
+    representatives plus n_random uniform nodes (node id = sum z_k m^k)."""
+    reps = []
+    for cls in np.ndindex(*([3] * d)):
+        z = [0 if c == 0 else (m - 1 if c == 2 else int(rng.integers(1, m - 1))) for c in cls]
+        reps.append(sum(zk * m ** k for k, zk in enumerate(z)))
+    rnd = rng.choice(m ** d, size=n_random, replace=False)
+    return np.unique(np.concatenate([np.asarray(reps), rnd]))
+
+
+@pytest.mark.parametrize("l", [(1, 7), (7, 1)])
+def test_apply_strip_operator_full_size_extreme_grids(l):
+    """configs[4] (L=8): the extreme grids (1,7) and (7,1) (58 M DOF each: moment pass 1 +
+    whole-x pass 2, stencil pass 1 + TMA pass 2) element by element on >= 10^4 sampled
+    outputs (every x-row x ~400 v-rows, resp. ~400 x-rows x every v-row, all 3^d boundary
+    classes included); the oracle assembles the level-7 rows on the patches of the sampled
+    nodes (oracle/rows.py, pinned against whole assembly)."""
+    from oracle.rows import sampled_apply
+    from paper_2204_05988_b200 import Problem
+    g = Problem(get_config("c4_6d_stream"))
+    cfg, o = _full_size_oracle("c4_6d_stream", (1, 1))
+    rng = np.random.default_rng(17)
+    gi = _grid_index(g, l)
+    _, _, n1, n2 = g.grid_info(SET_ACTIVE, gi)
+    X = rng.standard_normal((1, n1, n2))
+    Yt = torch.empty(n1 * n2, dtype=torch.float64, device="cuda")
+    g.sg_apply_strip_operator(SET_ACTIVE, gi, torch.from_numpy(X.ravel()).cuda(), Yt)
+    Y = Yt.cpu().numpy().reshape(X.shape)
+    m_big = 2 * 2 ** 6 + 1
+    if l == (1, 7):
+        xr, vr = np.arange(n1), _sample_nodes(m_big, 3, 400, rng)
+    else:
+        xr, vr = _sample_nodes(m_big, 3, 400, rng), np.arange(n2)
+    assert len(xr) * len(vr) >= 10 ** 4
+    ref = sampled_apply(cfg, o.terms, l, X, xr, vr)
+    got = Y[:, xr][:, :, vr]
+    assert relmax(got, ref) <= 1e-12
+
+
+def test_apply_strip_operator_full_size_c3():
+    """configs[3] at its full size (L=11, dG(1), L-shaped x factor): the balanced grids (5,6)
+    and (6,5) (7.4 M and 6.9 M DOF) element by element."""
+    from paper_2204_05988_b200 import Problem
+    g = Problem(get_config("c3_4d_lshape"))
+    rng = np.random.default_rng(21)
+    for l in [(5, 6), (6, 5)]:
+        cfg, o = _full_size_oracle("c3_4d_lshape", l)
+        gi = _grid_index(g, l)
+        _, _, n1, n2 = g.grid_info(SET_ACTIVE, gi)
+        X = rng.standard_normal((2, n1, n2))
+        Yt = torch.empty(2 * n1 * n2, dtype=torch.float64, device="cuda")
+        g.sg_apply_strip_operator(SET_ACTIVE, gi, torch.from_numpy(X.ravel()).cuda(), Yt)
+        ref = o.apply_pair(o.terms, l, l, X)
+        assert relmax(Yt.cpu().numpy().reshape(X.shape), ref) <= 1e-12, l
+
+
+def test_full_size_c1_every_grid_and_one_strip():
+    """configs[1] at its full size (L=14, 491 K active DOF, dG(1)): the strip operator on every
+    active and coarse grid element by element, and one strip (rhs from the interpolated u0,
+    the strip solve, the trace) against the oracle's direct-LU Richardson at rtol 1e-13."""
+    from oracle.sgrid import SGProblem
+    from paper_2204_05988_b200 import Problem
+    cfg = get_config("c1_2d_rot")
+    g, o = Problem(cfg), SGProblem(cfg)
+    rng = np.random.default_rng(23)
+    for set_, grids in ((SET_ACTIVE, o.active), (SET_COARSE, o.coarse)):
+        for gi, l in enumerate(grids):
+            X = rng.standard_normal(o.shape(l))
+            Yt = torch.empty(X.size, dtype=torch.float64, device="cuda")
+            g.sg_apply_strip_operator(set_, gi, torch.from_numpy(X.ravel()).cuda(), Yt)
+            assert relmax(Yt.cpu().numpy().reshape(X.shape), o.apply_diag(l, X)) <= 1e-12, (set_, l)
+    tr_ref, _, _ = o.run(nsteps=1, rtol=1e-13)
+    u0 = torch.zeros(g.set_size(SET_ACTIVE, 1), dtype=torch.float64, device="cuda")
+    g.sg_interp_u0(u0)
+    g.sg_step(1, 1, u0, rtol=1e-13, inner_rtol=1e-13)
+    assert relmax(_full(o, to_blocks(g, u0, S=1)), _full(o, tr_ref)) <= 1e-9
 
 
 def test_apply_strip_operator_full_size_4d():
     """configs[2] at its full size (L=12, bench launch configuration): the balanced grid (6,6)
     (17.9 M DOF, TMA pass 2 + moment pass 1) element by element against the oracle's exact
     factor matrices on its own level-6 meshes."""
-    from oracle.sgrid import SGProblem
     from paper_2204_05988_b200 import Problem
-    from oracle.problem import strip_terms
-    cfg = get_config("c2_4d_stream")
-    g = Problem(cfg)
-    gi = [i for i in range(g.num_grids(SET_ACTIVE)) if g.grid_info(SET_ACTIVE, i)[:2] == (6, 6)][0]
+    g = Problem(get_config("c2_4d_stream"))
+    gi = _grid_index(g, (6, 6))
     l1, l2, n1, n2 = g.grid_info(SET_ACTIVE, gi)
-    o = SGProblem(get_config("c2_4d_stream", L=7), galerkin="direct")   # meshes up to level 6
-    o.tau, o.delta = cfg["tau"], g.delta
-    o.terms = strip_terms(cfg, cfg["tau"], g.delta)
+    cfg, o = _full_size_oracle("c2_4d_stream", (6, 6))
     rng = np.random.default_rng(12)
     X = rng.standard_normal((1, n1, n2))
     Yt = torch.empty(n1 * n2, dtype=torch.float64, device="cuda")
     g.sg_apply_strip_operator(SET_ACTIVE, gi, torch.from_numpy(X.ravel()).cuda(), Yt)
     ref = o.apply_pair(o.terms, (6, 6), (6, 6), X)
     assert relmax(Yt.cpu().numpy().reshape(X.shape), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("name", CONFIG_ORDER)
+def test_step_at_bench_settings(name):
+    """sg_step at the settings bench.py times (outer rtol 1e-10, inner block solves to 1e-2)
+    against the oracle's direct-LU Richardson at rtol 1e-13: 3 strips, the 1e-9 bar."""
+    g, o = pair(name)
+    nst = 3
+    tr_ref, _, _ = o.run(nsteps=nst, rtol=1e-13)
+    u0 = torch.zeros(g.set_size(SET_ACTIVE, 1), dtype=torch.float64, device="cuda")
+    g.sg_interp_u0(u0)
+    g.reset_stats()
+    g.sg_step(1, nst, u0, rtol=1e-10, inner_rtol=1e-2)
+    assert relmax(_full(o, to_blocks(g, u0, S=1)), _full(o, tr_ref)) <= 1e-9
+    h = g.health()
+    assert h["outer_unconverged"] == 0 and h["outer_nonfinite"] == 0 and h["inner_maxit"] == 0, h
+
+
+@pytest.mark.parametrize("name,L", [("c0_2d_const", 6), ("c1_2d_rot", 5)])
+def test_final_time(name, L):
+    """All N = round(T/tau) strips to the final time T (configs[0]: 32 strips at its full
+    L = 6; configs[1]: 402 strips at L = 5) against the oracle's solution at T
+    (tests/golden/final_*.npz, written by tools/make_golden_final.py, which calls only
+    oracle/): relative L2-on-the-full-grid bar 1e-9 (north_star)."""
+    import os
+    from oracle.sgrid import SGProblem
+    from paper_2204_05988_b200 import Problem
+    cfg = get_config(name, L=L)
+    path = os.path.join(os.path.dirname(__file__), "golden", f"final_{name}_L{L}.npz")
+    ref = np.load(path)
+    o = SGProblem(cfg)
+    N = int(round(cfg["T"] / cfg["tau"]))
+    assert int(ref["nsteps"]) == N
+    g = Problem(cfg)
+    u = torch.zeros(g.set_size(SET_ACTIVE, 1), dtype=torch.float64, device="cuda")
+    g.sg_interp_u0(u)
+    g.sg_step(1, N, u, rtol=1e-13, inner_rtol=1e-13)
+    got = to_blocks(g, u, S=1)
+    blocks = {l: ref[f"block_{l[0]}_{l[1]}"] for l in o.active}
+    diff = {l: got[l] - blocks[l] for l in o.active}
+    # L2(Omega) norm of the function difference (representation independent, sec. 4.1)
+    err = o.spatial_l2(diff) / o.spatial_l2(blocks)
+    assert err <= 1e-9, err
+    assert relmax(_full(o, got), ref["full"]) <= 1e-9
