@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--secondary", default="c2_4d_stream",
+                    help="second workload measured in the same run (configs[2], the largest); 'none' to skip")
+    ap.add_argument("--secondary-steps", type=int, default=2)
     return ap.parse_args()
 
 
@@ -166,23 +169,34 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def main():
-    args = parse()
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        return run_reference(args, rank, world)
+def fp64_peak():
+    """Measured FP64 peaks of this GPU: tools/fp64_peak (DFMA register chains on every SM and
+    DMMA mma.sync.m8n8k4), run live; fallback: the committed profiles/fp64_peak.json of an
+    earlier run on this pool; last resort: derived from the guide's unit counts."""
+    exe = os.path.join(ROOT, "tools", "fp64_peak")
+    try:
+        out = subprocess.check_output([exe], timeout=60).decode().strip().splitlines()[-1]
+        d = json.loads(out)
+        d["source"] = "tools/fp64_peak, measured live on this GPU (" + d.get("how", "") + ")"
+        return d
+    except Exception:
+        pass
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+        d["source"] = "profiles/fp64_peak.json (tools/fp64_peak on an earlier box of this pool)"
+        return d
+    except Exception:
+        sm_max = (peaks().get("sm_max_mhz") or 1965.0) / 1e3
+        return {"dfma_tflops": 148 * 64 * 2 * sm_max / 1e3, "source": "derived: 148 SM x 64 FMA/clk x 2 x sm_max"}
+
+
+def measure(args, cfg, world, steps, warmup, e2e_steps, timing=True):
+    """Warm up, then time `steps` strips of the workload (device events on the handle's stream,
+    barrier + synchronize on both sides, max over ranks).  Strips run in order j = 1..N
+    (N = round(T/tau)) and start again from the interpolated u0 after the final time T."""
     import torch
     import torch.distributed as dist
     from paper_2204_05988_b200 import Problem
-    from sginputs import get_config
-
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg_over = {} if args.L is None else {"L": args.L}
-    cfg = get_config(args.config, **cfg_over)
     stream = torch.cuda.current_stream()
     t_setup = time.perf_counter()
     prob = Problem(cfg, stream=stream)
@@ -191,35 +205,50 @@ def main():
     N = int(round(cfg["T"] / cfg["tau"]))
     n_tr = prob.set_size(0, 1)
     trace = torch.zeros(n_tr, dtype=torch.float64, device="cuda")
+    state = {"j": 1}
+
+    def one_strip(tr, host=False):
+        if state["j"] > N:                  # past T: the next run of the workload starts at u0
+            state["j"] = 1
+            if host:
+                t = torch.zeros(n_tr, dtype=torch.float64, device="cuda")
+                prob.sg_interp_u0(t)
+                tr[:] = t.cpu().numpy()
+            else:
+                prob.sg_interp_u0(tr)
+        prob.sg_step(state["j"], 1, tr, args.rtol, args.inner_rtol)
+        state["j"] += 1
+
     prob.sg_interp_u0(trace)
-    j = 1
-    # warmup strips
-    for _ in range(args.warmup):
-        prob.sg_step(j, 1, trace, args.rtol, args.inner_rtol)
-        j += 1
+    for _ in range(warmup):
+        one_strip(trace)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     prob.reset_stats()
-    prob.set_timing(True)
+    prob.set_timing(timing)
+    j_first = state["j"]
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
-        for _ in range(args.steps):
-            prob.sg_step(j, 1, trace, args.rtol, args.inner_rtol)
-            j += 1
+        for _ in range(steps):
+            one_strip(trace)
         ev1.record(stream)
         torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     ms = ev0.elapsed_time(ev1)
     st = prob.stats()
     kt = prob.kernel_time()
+    health = prob.health()
     prob.set_timing(False)
     ms_max, dof_all = combine_ranks(ms, float(st["dof_applied"]), world, device="cuda")
-    value = dof_all / (ms_max / 1e3)
+    res = {"ms": ms, "ms_max": ms_max, "dof_all": dof_all, "stats": st, "kt": kt, "health": health,
+           "clocks": clk.summary(), "setup_s": t_setup, "N": N, "strips": [j_first, state["j"] - 1],
+           "prob": prob, "n_tr": n_tr}
     # ------------------------------------------------------------- e2e (host buffers)
-    e2e = None
-    if not args.no_e2e:
+    if e2e_steps > 0:
         import numpy as np
         host = torch.empty(n_tr, dtype=torch.float64).pin_memory()
         host.copy_(trace)
@@ -227,10 +256,8 @@ def main():
         prob.reset_stats()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        je = j - args.e2e_steps
-        for _ in range(args.e2e_steps):
-            prob.sg_step(je, 1, hnp, args.rtol, args.inner_rtol)   # H2D trace, strip, D2H trace
-            je += 1
+        for _ in range(e2e_steps):
+            one_strip(hnp, host=True)       # sg_step(host trace): H2D trace, strip, D2H trace
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if world > 1:
@@ -239,55 +266,119 @@ def main():
             dt = float(t[0])
         st2 = prob.stats()
         dof2 = float(st2["dof_applied"]) * world
-        e2e = {"value": dof2 / dt, "unit": "DOF-applies/s", "h2d_bytes_per_step": 8 * n_tr,
-               "d2h_bytes_per_step": 8 * n_tr, "time_steps_per_s": args.e2e_steps * world / dt,
-               "steps": args.e2e_steps, "note": "sg_step(host trace): H2D trace, strip solve, D2H trace; host wall clock"}
-    # ---------------------------------------------------------------- roofline
+        res["e2e"] = {"value": dof2 / dt, "unit": "DOF-applies/s", "h2d_bytes_per_step": 8 * n_tr,
+                      "d2h_bytes_per_step": 8 * n_tr, "time_steps_per_s": e2e_steps * world / dt,
+                      "steps": e2e_steps,
+                      "note": "sg_step(host trace): H2D trace, strip solve, D2H trace; host wall clock"}
+    return res
+
+
+def roofline(res, cfg, fp):
+    """Roofline of the strip-operator apply (one 'launch' = one apply on one component grid,
+    all its kernels), from the device timestamps around every apply inside the timed region."""
+    kt, st, ms = res["kt"], res["stats"], res["ms"]
     pk = peaks()
     hbm = pk.get("hbm_gbs", 6650.0)
-    # fp64 peak from the unit counts of the guides: 148 SMs x 64 FP64 FMA/clk x 2 FLOP x max SM clock
-    sm_max = (pk.get("sm_max_mhz") or 1965.0) / 1e3
-    fp64_peak_tflops = 148 * 64 * 2 * sm_max / 1e3
-    achieved_tf = (kt["flops"] / 1e12) / (kt["ms"] / 1e3) if kt["ms"] > 0 else None
-    achieved_gbs = (kt["bytes"] / 1e9) / (kt["ms"] / 1e3) if kt["ms"] > 0 else None
-    roof = {"bound": "alu", "achieved": achieved_tf, "peak": fp64_peak_tflops, "unit": "TFLOP/s",
-            "frac": (achieved_tf / fp64_peak_tflops) if achieved_tf else None, "traffic": None,
-            "kernel": ("strip-operator apply per component grid: pass 1 along v (k_vfan_st on 3D v-lattices, "
-                       "k_vmom shifted moments on 2D) + pass 2 along x (k_xfanin_tma TMA-pipelined line sweep, "
-                       "k_xwhole on level-1/2 x-lattices); CUDA events around every apply"),
-            "peak_source": "derived fp64: 148 SM x 64 FMA/clk x 2 x sm_max_mhz (DESIGN.md sec. 5)",
-            "algorithmic_flops_per_launch": kt["flops"] / max(kt["launches"], 1),
+    peak_tf = fp["dfma_tflops"]
+    sec = kt["ms"] / 1e3
+    achieved_tf = (kt["flops"] / 1e12) / sec if sec > 0 else None
+    achieved_gbs = (kt["bytes"] / 1e9) / sec if sec > 0 else None
+    n_ap = max(kt["launches"], 1)
+    roof = {"bound": "alu", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+            "frac": (achieved_tf / peak_tf) if achieved_tf else None, "traffic": None,
+            "kernel": ("strip-operator apply per component grid (all its kernels): pass 1 along v (k_vmom "
+                       "shifted moments / k_vfan_st stencils) + pass 2 along x (k_xfanin_tma TMA line sweep, "
+                       "k_xwhole, k_xgat_st, k_gather_s2); device globaltimer stamps around every apply"),
+            "peak_source": "FP64 DFMA pipe, " + fp.get("source", ""),
+            "flops_note": "2 FLOP per multiply-add on the structural nonzeros of the factor matrices "
+                          "(|a_ij| > 1e-12 max|a|), face groups on boundary rows only (DESIGN.md sec. 5)",
+            "algorithmic_flops_per_launch": kt["flops"] / n_ap,
+            "algorithmic_bytes_per_launch": kt["bytes"] / n_ap,
+            "dof_per_launch": float(st["dof_applied"]) / max(st["applies"], 1),
             "hbm_view": {"achieved_gbs": achieved_gbs, "peak_gbs": hbm,
                          "frac": (achieved_gbs / hbm) if achieved_gbs else None,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback 6650 GB/s",
-                         "note": "algorithmic bytes = read X + write Y + factor values/patterns"},
-            "traffic_note": "per-launch DRAM bytes from ncu --set full in profiles/ (per grid)",
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in pk
+                         else "fallback 6650 GB/s",
+                         "note": "algorithmic bytes = read X + write Y + the factor data the launched kernels "
+                                 "read (class tables / per-column coefficients / ELL arrays)"},
+            "dmma_peak_tflops": fp.get("dmma_tflops"),
             "share_of_step": (kt["ms"] / ms) if ms > 0 else None,
-            "avg_apply_ms": kt["ms"] / max(st["applies"], 1)}
+            "avg_apply_ms": kt["ms"] / n_ap}
     tr = apply_traffic(cfg["name"])
     if tr and st["applies"]:
         dof_per_apply = float(st["dof_applied"]) / st["applies"]
         roof["traffic"] = tr["dram_bytes_per_dof"] * dof_per_apply
         roof["traffic_note"] = ("ncu dram__bytes_read.sum + dram__bytes_write.sum of the apply kernels, "
-                                "%.1f B per DOF-apply (%s) x %.0f DOF per apply of this run; algorithmic: %.1f B"
-                                % (tr["dram_bytes_per_dof"], tr["source"], dof_per_apply,
-                                   kt["bytes"] / max(kt["launches"], 1)))
-    clocks = clk.summary()
-    out = {"metric": METRIC, "value": value, "unit": "DOF-applies/s", "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                                "%.1f B per DOF-apply (%s) x %.0f DOF per apply of this run"
+                                % (tr["dram_bytes_per_dof"], tr["source"], dof_per_apply))
+    return roof
+
+
+def summary(res, cfg, fp, world, steps):
+    st = res["stats"]
+    value = res["dof_all"] / (res["ms_max"] / 1e3)
+    prob = res["prob"]
+    return {"value": value, "ms_per_step": res["ms_max"] / steps,
+            "time_steps_per_s": steps * world / (res["ms_max"] / 1e3),
+            "config": {"workload": cfg["name"], "L": cfg["L"], "d": cfg["d"], "q": cfg["q"], "tau": cfg["tau"],
+                       "strips_total": res["N"], "strips_timed": res["strips"],
+                       "strips_note": "strips j run in order 1..N (N = round(T/tau)); after T the workload "
+                                      "restarts from the interpolated u0",
+                       "parallelism": f"replicas{world}",
+                       "l2": "inputs larger than L2 (component grids up to %.0f MB)" % (
+                           max(prob.grid_info(0, g)[2] * prob.grid_info(0, g)[3] for g in range(prob.num_grids(0)))
+                           * 8 * prob.S / 1e6),
+                       "dof_active": prob.set_size(0, prob.S)},
+            "gpu_launches": st["launches"], "applies": st["applies"], "outer_iters": st["outer_iters"],
+            "inner_iters": st["inner_iters"], "outer_mr_switches": st.get("outer_mr_switches"),
+            "solver_health": res["health"],
+            "setup_s": res["setup_s"], "roofline": roofline(res, cfg, fp), "clocks": res["clocks"]}
+
+
+def main():
+    args = parse()
+    if args.secondary == "none":
+        args.secondary = None
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    import torch
+    import torch.distributed as dist
+    from sginputs import get_config
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    fp = fp64_peak()
+    cfg_over = {} if args.L is None else {"L": args.L}
+    cfg = get_config(args.config, **cfg_over)
+    res = measure(args, cfg, world, args.steps, args.warmup, 0 if args.no_e2e else args.e2e_steps)
+    sm = summary(res, cfg, fp, world, args.steps)
+    flagged = any(v for v in res["health"].values())
+    out = {"metric": METRIC, "value": sm["value"], "unit": "DOF-applies/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": sm["ms_per_step"], "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": cfg["name"], "L": cfg["L"], "d": cfg["d"], "q": cfg["q"], "tau": cfg["tau"],
-                      "strips_total": N, "parallelism": f"replicas{world}",
-                      "l2": "inputs larger than L2 (component grids up to %.0f MB)" % (
-                          max(prob.grid_info(0, g)[2] * prob.grid_info(0, g)[3] for g in range(prob.num_grids(0)))
-                          * 8 * prob.S / 1e6),
-                      "rtol": args.rtol, "inner_rtol": args.inner_rtol,
-                      "dof_active": prob.set_size(0, prob.S)},
-           "time_steps_per_s": args.steps * world / (ms_max / 1e3),
-           "gpu_launches": st["launches"],
-           "applies": st["applies"], "outer_iters": st["outer_iters"], "inner_iters": st["inner_iters"],
-           "outer_mr_switches": st.get("outer_mr_switches"),
-           "setup_s": t_setup, "roofline": roof, "clocks": clocks, "e2e": e2e}
+           "config": dict(sm["config"], rtol=args.rtol, inner_rtol=args.inner_rtol),
+           "time_steps_per_s": sm["time_steps_per_s"],
+           "gpu_launches": sm["gpu_launches"], "applies": sm["applies"], "outer_iters": sm["outer_iters"],
+           "inner_iters": sm["inner_iters"], "outer_mr_switches": sm["outer_mr_switches"],
+           "solver_health": sm["solver_health"], "flagged_unconverged": flagged,
+           "setup_s": sm["setup_s"], "roofline": sm["roofline"], "clocks": sm["clocks"], "e2e": res.get("e2e")}
+    del res
+    # configs[2] (the largest configuration by DOF) measured in the same run, fewer strips
+    if args.secondary and args.secondary != args.config and world == 1:
+        try:
+            cfg2 = get_config(args.secondary)
+            r2 = measure(args, cfg2, world, args.secondary_steps, 1, 0)
+            s2 = summary(r2, cfg2, fp, world, args.secondary_steps)
+            s2["steps"], s2["warmup"] = args.secondary_steps, 1
+            s2["solver_health"] = r2["health"]
+            out["secondary"] = {args.secondary: s2}
+            del r2
+        except Exception as ex:
+            out["secondary"] = {args.secondary: {"error": str(ex)}}
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             out["cpu_baseline"] = cpu_baseline(cfg["name"])

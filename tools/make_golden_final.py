@@ -6,6 +6,7 @@ input module sginputs/ (no CUDA path).
 
   python tools/make_golden_final.py c0_2d_const 6
   python tools/make_golden_final.py c1_2d_rot 5
+  python tools/make_golden_final.py c1_2d_rot 14 1     # first strip only (full-size configs[1])
 """
 import os
 import sys
@@ -20,20 +21,21 @@ from oracle.sgrid import SGProblem  # noqa: E402
 from sginputs import get_config  # noqa: E402
 
 
-def main(name, L):
+def main(name, L, nsteps=None):
     cfg = get_config(name, L=L)
     o = SGProblem(cfg)
-    N = int(round(cfg["T"] / cfg["tau"]))
+    N = int(round(cfg["T"] / cfg["tau"])) if nsteps is None else nsteps
     t0 = time.time()
     tr, _, its = o.run(nsteps=N, rtol=1e-13)
     out = {"nsteps": N, "full": o.to_full(tr), "iters": np.asarray(its)}
     for (l1, l2), u in tr.items():
         out[f"block_{l1}_{l2}"] = u
-    path = os.path.join(ROOT, "tests", "golden", f"final_{name}_L{L}.npz")
+    tag = "final" if nsteps is None else f"strips{nsteps}"
+    path = os.path.join(ROOT, "tests", "golden", f"{tag}_{name}_L{L}.npz")
     np.savez_compressed(path, **out)
     print(f"{path}: {N} strips in {time.time() - t0:.1f}s, outer its {min(its)}-{max(its)}, "
           f"||U(T)|| = {o.spatial_l2(tr):.6e}")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]))
+    main(sys.argv[1], int(sys.argv[2]), int(sys.argv[3]) if len(sys.argv) > 3 else None)
