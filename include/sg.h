@@ -202,6 +202,9 @@ int sg_reset_stats(sg_problem* P);
  * iteration switched to residual-minimising step lengths because the update
  * norm grew (safeguard, reading R13); SG_OUTER=1 disables it */
 int sg_outer_switches(sg_problem* P, int64_t* switches);
+/* Update norms ||du||_{L2(I_j x Omega)} and step lengths omega of every outer iteration of
+ * the last strip solve (at most 256); *n = its iteration count (host arrays, may be NULL). */
+int sg_solve_history(sg_problem* P, int max_n, double* nd, double* omega, int* n);
 /* Timing mode: device timestamps (globaltimer, in the captured graphs too) bracket every
  * strip-operator apply; sg_kernel_time returns the summed device time (ms) of the applies
  * that did work (converged grids excluded), their count, their algorithmic bytes (read X +

@@ -92,6 +92,7 @@ def load_library():
         "sg_stats": (I, [P, pI64, pI64, pI64, pI64, pI64]),
         "sg_solver_health": (I, [P, pI64, pI64, pI64, pI64]),
         "sg_outer_switches": (I, [P, pI64]),
+        "sg_solve_history": (I, [P, I, pD, pD, pI]),
         "sg_reset_stats": (I, [P]),
         "sg_set_timing": (I, [P, I]),
         "sg_kernel_time": (I, [P, pD, pI64, pD, pD]),
@@ -351,6 +352,14 @@ class Problem:
         _check(self.lib.sg_solver_health(self.h, *[C.byref(x) for x in v]))
         return dict(zip(["outer_unconverged", "outer_nonfinite", "inner_maxit", "inner_breakdowns"],
                         [x.value for x in v]))
+
+    def solve_history(self):
+        """(update norms, step lengths) of every outer iteration of the last strip solve."""
+        nd = (C.c_double * 256)()
+        om = (C.c_double * 256)()
+        n = C.c_int()
+        _check(self.lib.sg_solve_history(self.h, 256, nd, om, C.byref(n)))
+        return list(nd[:n.value]), list(om[:n.value])
 
     def reset_stats(self):
         _check(self.lib.sg_reset_stats(self.h))

@@ -56,6 +56,8 @@ extern "C" int sg_create(const sg_config* cfg, void* stream, sg_problem** out) {
     P->use_graphs = getenv("SG_NO_GRAPHS") == nullptr;
     // fallback of the TMA line sweep (register line sweep k_xfanin)
     P->use_tma = getenv("SG_NO_TMA") == nullptr;
+    // fused whole-x apply on the tiny x-lattices (fallback: moment pass 1 + whole-x pass 2)
+    P->use_fused = getenv("SG_NO_FUSED") == nullptr;
     // fallback of the batched cross-grid lower part (also taken when its buffers do not fit)
     P->use_cross_batched = getenv("SG_NO_CROSS_BATCH") == nullptr;
     // outer step length (reading R13): 0 Richardson + MR safeguard, 1 plain, 2 MR always
@@ -216,8 +218,15 @@ extern "C" void sg_destroy(sg_problem* P) {
     for (double* t : P->xfi_itab) cudaFree(t);
     for (double* t : P->vm_tab) cudaFree(t);
     for (double* t : P->xw_dev) cudaFree(t);
+    for (double* t : P->fw_dev) cudaFree(t);
     for (int* t : P->vm_blist) cudaFree(t);
     solver_destroy(P);
+    for (auto s : P->cx_streams) cudaStreamDestroy(s);
+    for (auto e : P->ev_cx_join) cudaEventDestroy(e);
+    for (auto w : P->cx_ws) cudaFree(w);
+    for (auto w : P->cx_h) cudaFree(w);
+    for (auto w : P->cx_y) cudaFree(w);
+    if (P->ev_cx_fork) cudaEventDestroy(P->ev_cx_fork);
     for (double* v : P->vec) cudaFree(v);
     cudaFree(P->trace_dev);
     cudaFree(P->dinv);
@@ -490,6 +499,19 @@ extern "C" int sg_kernel_time(sg_problem* P, double* ms, int64_t* launches, doub
     if (launches) *launches = c ? c->timed_applies : 0;
     if (alg_bytes) *alg_bytes = c ? c->alg_bytes : 0.0;
     if (alg_flops) *alg_flops = c ? c->alg_flops : 0.0;
+    return SG_OK;
+}
+
+extern "C" int sg_solve_history(sg_problem* P, int max_n, double* nd, double* omega, int* n) {
+    CHECK_ARG(P && n && max_n >= 0, "null argument");
+    SG_TRY(sync_stats(P));
+    const SolveCtl* c = P->hctl;
+    const int it = c ? std::min(c->it, 256) : 0;
+    *n = it;
+    for (int i = 0; i < std::min(it, max_n); ++i) {
+        if (nd) nd[i] = c->hist_nd[i];
+        if (omega) omega[i] = c->hist_om[i];
+    }
     return SG_OK;
 }
 

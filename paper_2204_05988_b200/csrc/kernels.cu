@@ -272,6 +272,30 @@ int launch_copy(sg_problem* P, int64_t n, const double* x, double* y) {
     SG_CUDA(cudaMemcpyAsync(y, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, P->stream));
     return SG_OK;
 }
+struct SumList {
+    int k;
+    const double* x[MAX_SUM];
+};
+__global__ void k_sum_into(int64_t n, SumList sl, double* __restrict__ y) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double v = y[i];
+        for (int j = 0; j < sl.k; ++j) v += sl.x[j][i];
+        y[i] = v;
+    }
+}
+// y += sum_j xs[j]
+int launch_sum_into(sg_problem* P, int64_t n, int k, double* const* xs, double* y) {
+    if (k > MAX_SUM) return SG_ERR_UNSUPPORTED;
+    SumList sl;
+    sl.k = k;
+    for (int j = 0; j < k; ++j) sl.x[j] = xs[j];
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16));
+    k_sum_into<<<blocks, 256, 0, P->stream>>>(n, sl, y);
+    P->launches++;
+    SG_CUDA(cudaGetLastError());
+    return SG_OK;
+}
+
 int launch_zero(sg_problem* P, int64_t n, double* y) {
     if (n == 0) return SG_OK;
     SG_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * n, P->stream));

@@ -191,8 +191,10 @@ struct SolveCtl {
     long long inner_breakdowns, inner_maxit, outer_unconverged, outer_nonfinite;
     long long n_applies, timed_applies;
     double dof_applied, alg_bytes, alg_flops, apply_ns;
-    unsigned long long t0;
+    unsigned long long t0[64];       // per-slot start stamps (concurrent applies)
     int act[64];                     // grid active in the current inner iteration
+    double hist_nd[256];             // ||du|| of every outer iteration of the last strip solve
+    double hist_om[256];             // its step length omega
 };
 
 struct Grid {
@@ -244,6 +246,23 @@ struct sg_problem {
     bool capturing = false;        // enqueueing into a strip-solve graph
     bool in_solve = false;         // applies are counted on the device (inner control kernel)
     std::vector<cudaStream_t> cap_streams;   // capture streams of nested conditional bodies
+    // concurrent per-grid applies in the block solver (small configurations, launch-latency bound):
+    // one stream and one private intermediate workspace per solve grid
+    bool par_applies = false;
+    // concurrent cross-grid transfer chains (one branch per group, small configurations)
+    bool par_cross = false;
+    std::vector<cudaStream_t> cx_streams;
+    std::vector<double*> cx_ws, cx_h, cx_y;
+    size_t cx_ws_n = 0;
+    int64_t cx_h_n = 0, cx_y_n = 0;
+    cudaEvent_t ev_cx_fork = nullptr;
+    std::vector<cudaEvent_t> ev_cx_join;
+    int stamp_slot = 63;           // timestamp slot of the apply being enqueued
+    std::vector<cudaStream_t> par_streams;
+    std::vector<double*> par_ws;
+    std::vector<size_t> par_ws_n;
+    cudaEvent_t ev_fork = nullptr;
+    std::vector<cudaEvent_t> ev_join;
     struct SolveGraph {
         const double *b, *u;
         double rtol, inner_rtol;
@@ -265,6 +284,10 @@ struct sg_problem {
     std::vector<double*> xw_tab;   // non-null when the whole-x tables exist
     std::vector<double*> xw_dev;
     std::vector<int> xw_np;
+    // fused whole-x apply (tiny x-lattices): [g][pair] tables per x-level, SG_NO_FUSED disables
+    std::vector<double*> fw_dev;
+    int fw_np = 0;
+    bool use_fused = true;
     // batched cross-grid lower part: stage-0 fan-outs of all v-groups and the Horner
     // results per target and group (even pitch); also used by the batched upper part
     double* cross_q = nullptr;
@@ -306,6 +329,8 @@ int launch_gather(sg_problem* P, int dir, int W, int S_out, int64_t n1_in, int64
 int launch_axpby(sg_problem* P, int64_t n, double a, const double* x, double b, double* y);
 int launch_copy(sg_problem* P, int64_t n, const double* x, double* y);
 int launch_zero(sg_problem* P, int64_t n, double* y);
+constexpr int MAX_SUM = 32;
+int launch_sum_into(sg_problem* P, int64_t n, int k, double* const* xs, double* y);
 int launch_ell_to_stencil(sg_problem* P, int64_t n, int W, const int32_t* cols, const double* vals,
                           const StencilOff& so, double* out);
 int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, const uint8_t* xflag,
@@ -324,6 +349,9 @@ int launch_xfanin(sg_problem* P, int l1, int64_t n1, int64_t n2, const double* Z
                   double beta);
 int launch_xwhole(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pitch, const double* Z, int64_t gstride,
                   double* Y);
+int prepare_fwhole(sg_problem* P);
+
+int launch_fwhole(sg_problem* P, int l1, int l2, int64_t n2, const double* X, double* Y);
 // vmoment.cu
 int prepare_vmom(sg_problem* P);
 int launch_vmom(sg_problem* P, int l2, int64_t nrows, int64_t n2, int64_t pitch, const double* X, double* const* outs,
@@ -355,6 +383,6 @@ int step(sg_problem* P, int j0, int nsteps, double* trace_dev, double rtol, doub
 int rhs(sg_problem* P, int j, const double* trace, double* b);
 int trace_of(sg_problem* P, const double* u, double* tr);
 int interp_u0(sg_problem* P, double* u);
-__global__ void k_tstamp(SolveCtl* c, const double* skip, int phase, double bytes, double flops);
+__global__ void k_tstamp(SolveCtl* c, const double* skip, int slot, int phase, double bytes, double flops);
 int prepare_stencils(sg_problem* P);
 }  // namespace sg

@@ -19,6 +19,7 @@ int64_t set_size(const sg_problem* P, int set, int S) {
 }
 
 static inline int64_t gsize(const Grid& g) { return g.n1 * g.n2; }
+constexpr int VMT_NR = 16;   // rows of a moment class table (10 monomials + 6 chi groups)
 
 // generic pass 2 on box x-lattices (band kernel over the stencil-format matrices)
 static int xgather(sg_problem* P, const Grid& g, const XgatParams& ep, double* Y, double beta) {
@@ -130,6 +131,17 @@ static int apply_diag_impl(sg_problem* P, const Grid& g, const double* X, double
     const int nb = (int)P->vorder.size();
     const bool vbox = P->fv.kind == SG_MESH_BOX && nb <= MAXG;
     const bool xbox = P->fx.kind == SG_MESH_BOX;
+    // ---- fused single pass (tiny x-lattices): no intermediates
+    {
+        const int rc = launch_fwhole(P, g.l1, g.l2, g.n2, X, Y);
+        if (rc == SG_OK) {
+            int ncls = 1;
+            for (int q = 0; q < P->fv.d; ++q) ncls *= 3;
+            *fbytes += 8.0 * (ncls * (VMT_NR * P->fv.W) + 16.0 * 223);   // moment class table + x table
+            return SG_OK;
+        }
+        if (rc != SG_ERR_UNSUPPORTED) return rc;
+    }
     // ---- pass 1: Z_b = (Id x Id x B_b) X for every v-group b (interior groups first)
     // (TMA pass 2 reads the intermediates with an even row pitch)
     const bool tma2 = vbox && xbox && S == 1 && l_has_xfi(P, g.l1);
@@ -211,7 +223,7 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y, const d
     const int S = P->S;
     const int64_t n = gsize(g);
     if (P->timing) {
-        k_tstamp<<<1, 1, 0, P->stream>>>(P->ctl, skip, 0, 0.0, 0.0);
+        k_tstamp<<<1, 1, 0, P->stream>>>(P->ctl, skip, P->stamp_slot, 0, 0.0, 0.0);
         P->launches++;
     }
     P->skip = skip;
@@ -220,7 +232,8 @@ int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y, const d
     P->skip = nullptr;
     if (rc != SG_OK) return rc;
     if (P->timing) {
-        k_tstamp<<<1, 1, 0, P->stream>>>(P->ctl, skip, 1, 16.0 * S * (double)n + fbytes, diag_flops(P, g));
+        k_tstamp<<<1, 1, 0, P->stream>>>(P->ctl, skip, P->stamp_slot, 1, 16.0 * S * (double)n + fbytes,
+                                           diag_flops(P, g));
         P->launches++;
         SG_CUDA(cudaGetLastError());
     }
@@ -405,6 +418,7 @@ int prepare_stencils(sg_problem* P) {
     }
     SG_TRY(prepare_xfanin(P));
     SG_TRY(prepare_vmom(P));
+    SG_TRY(prepare_fwhole(P));
     SG_CUDA(cudaStreamSynchronize(P->stream));
     return SG_OK;
 }
@@ -431,6 +445,36 @@ int apply_cross_prepare(sg_problem* P) {
     int rc = cross_lower_batched(P, nullptr, nullptr);   // allocation only (never inside a capture)
     if (rc != SG_OK && rc != SG_ERR_UNSUPPORTED) return rc;
     P->cross_batched_tried = true;
+    // concurrent per-group branches of the per-group (unbatched) path: the configurations whose
+    // cross-grid apply is a long chain of tiny launches (d = 1), when the private workspaces fit
+    const int nbr = (int)(P->vgroups.size() + P->xgroups.size());
+    const int64_t Na = set_size(P, SG_SET_ACTIVE, P->S);
+    const size_t per = P->wsZ_n + 3 * (size_t)Na;
+    if (P->fx.d == 1 && P->fv.d == 1 && getenv("SG_SERIAL_CROSS") == nullptr && nbr <= MAX_SUM &&
+        per * nbr * sizeof(double) <= ((size_t)1 << 30)) {
+        SG_CUDA(cudaEventCreateWithFlags(&P->ev_cx_fork, cudaEventDisableTiming));
+        for (int i = 0; i < nbr; ++i) {
+            cudaStream_t s;
+            cudaEvent_t e;
+            double *w, *h, *y;
+            SG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            SG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            SG_CUDA(cudaMalloc(&w, sizeof(double) * P->wsZ_n));
+            SG_CUDA(cudaMalloc(&h, sizeof(double) * 2 * Na));
+            SG_CUDA(cudaMalloc(&y, sizeof(double) * Na));
+            SG_CUDA(cudaMemset(w, 0, sizeof(double) * P->wsZ_n));
+            P->cx_streams.push_back(s);
+            P->ev_cx_join.push_back(e);
+            P->cx_ws.push_back(w);
+            P->cx_h.push_back(h);
+            P->cx_y.push_back(y);
+        }
+        P->cx_ws_n = P->wsZ_n;
+        P->cx_h_n = 2 * Na;
+        P->cx_y_n = Na;
+        P->par_cross = true;
+        SG_CUDA(cudaDeviceSynchronize());
+    }
     return SG_OK;
 }
 
@@ -734,7 +778,42 @@ static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in
         else if (rc != SG_ERR_UNSUPPORTED) return rc;
     }
     const int nvg = lower_done ? 0 : (mass ? 1 : (int)P->vgroups.size());
+    // Concurrent groups (small configurations): every group's transfer chain and gathers run as
+    // an independent branch (own stream, chain and Horner workspaces, partial output), summed at
+    // the end; otherwise all groups run serially on the handle's stream into Y.
+    const int nxg_all = ng >= 2 ? (mass ? 1 : (int)P->xgroups.size()) : 0;
+    const bool par = P->par_cross && !lower_done && nvg + nxg_all <= (int)P->cx_streams.size() &&
+                     (int64_t)set_size(P, SG_SET_ACTIVE, S_out) <= P->cx_y_n &&
+                     (int64_t)set_size(P, SG_SET_ACTIVE, S_in) * 2 <= P->cx_h_n;
+    cudaStream_t main_stream = P->stream;
+    double* const wsZ0 = P->wsZ;
+    double* const wsH0 = P->wsH;
+    int nbranch = 0;
+    if (par) SG_CUDA(cudaEventRecord(P->ev_cx_fork, main_stream));
+    auto branch_begin = [&](double** Yd) -> int {
+        if (!par) {
+            *Yd = Y;
+            return SG_OK;
+        }
+        const int br = nbranch++;
+        P->stream = P->cx_streams[br];
+        SG_CUDA(cudaStreamWaitEvent(P->stream, P->ev_cx_fork, 0));
+        P->wsZ = P->cx_ws[br];
+        P->wsH = P->cx_h[br];
+        *Yd = P->cx_y[br];
+        return launch_zero(P, set_size(P, SG_SET_ACTIVE, S_out), *Yd);
+    };
+    auto branch_end = [&]() -> int {
+        if (!par) return SG_OK;
+        SG_CUDA(cudaEventRecord(P->ev_cx_join[nbranch - 1], P->stream));
+        P->stream = main_stream;
+        P->wsZ = wsZ0;
+        P->wsH = wsH0;
+        return SG_OK;
+    };
     for (int b = 0; b < nvg; ++b) {
+        double* Yd = Y;
+        SG_TRY(branch_begin(&Yd));
         const int vspec = mass ? P->mass_v : P->vgroups[b].spec;
         int64_t pos = 0;
         for (int pp = 1; pp <= ng; ++pp) {
@@ -745,7 +824,7 @@ static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in
                 pos += (int64_t)S_in * n1(lx) * n2(lv0 - k);
             }
         }
-        if ((size_t)pos > P->wsZ_n) {
+        if ((size_t)pos > (par ? P->cx_ws_n : P->wsZ_n)) {
             set_error("apply_cross: chain workspace too small");
             return SG_ERR_STATE;
         }
@@ -810,7 +889,7 @@ static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in
                     for (const auto& ce : P->vgroups[b].comb[p]) ep.e[ep.ne++] = {acc, ce.st, ce.s_out, ce.s_in, bo, 1.0, ce.ctab};
                 }
                 if (ep.ne) SG_TRY(launch_xgat_st(P, P->fx.d, S_out, n1(p), n2(lv), P->fx.lev[p].so, P->fx.lev[p].bflag, ep,
-                                                 Y + offOut[p - 1], 1.0, P->fx.lev[p].m));
+                                                 Yd + offOut[p - 1], 1.0, P->fx.lev[p].m));
             } else {
                 EntryList el;
                 el.ne = 0;
@@ -823,9 +902,10 @@ static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in
                     for (const auto& ce : P->vgroups[b].comb[p]) el.e[el.ne++] = {acc, ce.vals, 1.0, ce.s_out, ce.s_in};
                 }
                 if (el.ne) SG_TRY(launch_gather(P, 0, Wx, S_out, n1(p), n2(lv), n1(p), P->fx.lev[p].cols, el,
-                                                Y + offOut[p - 1], 1.0));
+                                                Yd + offOut[p - 1], 1.0));
             }
         }
+        SG_TRY(branch_end());
     }
     // ---------------- upper part (targets p < sources p')
     bool upper_done = false;
@@ -837,6 +917,8 @@ static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in
     if (ng >= 2 && !upper_done) {
         const int nxg = mass ? 1 : (int)P->xgroups.size();
         for (int a = 0; a < nxg; ++a) {
+            double* Yd = Y;
+            SG_TRY(branch_begin(&Yd));
             const int xspec = mass ? P->mass_x : P->xgroups[a].spec;
             int64_t pos = 0;
             for (int pp = 2; pp <= ng; ++pp) {
@@ -847,7 +929,7 @@ static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in
                     pos += (int64_t)S_in * n1(pp - k) * n2(lv);
                 }
             }
-            if ((size_t)pos > P->wsZ_n) {
+            if ((size_t)pos > (par ? P->cx_ws_n : P->wsZ_n)) {
                 set_error("apply_cross: chain workspace too small (upper)");
                 return SG_ERR_STATE;
             }
@@ -914,7 +996,7 @@ static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in
                         for (const auto& ce : P->xgroups[a].comb[lvt]) ep.e[ep.ne++] = {acc, ce.st, ce.s_out, ce.s_in, 0, 1.0};
                     }
                     if (ep.ne) SG_TRY(launch_vgat_st(P, P->fv.d, S_out, n1(p), n2(lvt), P->fv.lev[lvt].so, ep,
-                                                     Y + offOut[p - 1], 1.0));
+                                                     Yd + offOut[p - 1], 1.0));
                 } else {
                     EntryList el;
                     el.ne = 0;
@@ -927,10 +1009,15 @@ static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in
                         for (const auto& ce : P->xgroups[a].comb[lvt]) el.e[el.ne++] = {acc, ce.vals, 1.0, ce.s_out, ce.s_in};
                     }
                     if (el.ne) SG_TRY(launch_gather(P, 1, Wv, S_out, n1(p), n2(lvt), n2(lvt), P->fv.lev[lvt].cols, el,
-                                                    Y + offOut[p - 1], 1.0));
+                                                    Yd + offOut[p - 1], 1.0));
                 }
             }
+            SG_TRY(branch_end());
         }
+    }
+    if (par && nbranch > 0) {   // join the branches and sum their partial outputs
+        for (int i = 0; i < nbranch; ++i) SG_CUDA(cudaStreamWaitEvent(main_stream, P->ev_cx_join[i], 0));
+        SG_TRY(launch_sum_into(P, set_size(P, SG_SET_ACTIVE, S_out), nbranch, P->cx_y.data(), Y));
     }
     return SG_OK;
 }

@@ -478,6 +478,10 @@ __global__ void k_outer_end(SolveCtl* c, double rtol, int max_iter, int mode, Co
             c->outer_unconverged++;
         }
     }
+    if (c->it >= 1 && c->it <= 256) {
+        c->hist_nd[c->it - 1] = nd;
+        c->hist_om[c->it - 1] = om;
+    }
     c->nd_prev = nd;
     c->done = done;
     set_cond(cd.outer, cd.use, done == 0, &c->cond_outer);
@@ -522,18 +526,18 @@ __global__ void k_inner_ctl(SolveCtl* c, const double* scal, GridTab gt, int max
 // device timestamps around a strip-operator apply (timing mode): phase 0 start, phase 1 end
 // (accumulates the elapsed globaltimer ns and the apply's algorithmic bytes / FLOPs unless the
 // grid is converged, i.e. its kernels exited without work)
-__global__ void k_tstamp(SolveCtl* c, const double* skip, int phase, double bytes, double flops) {
+__global__ void k_tstamp(SolveCtl* c, const double* skip, int slot, int phase, double bytes, double flops) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (phase == 0) {
-        c->t0 = t;
+        c->t0[slot] = t;
         return;
     }
     if (skip && *skip != 0.0) return;
-    c->apply_ns += (double)(t - c->t0);
-    c->timed_applies++;
-    c->alg_bytes += bytes;
-    c->alg_flops += flops;
+    atomicAdd(&c->apply_ns, (double)(t - c->t0[slot]));   // (concurrent applies: atomics)
+    atomicAdd((unsigned long long*)&c->timed_applies, 1ull);
+    atomicAdd(&c->alg_bytes, bytes);
+    atomicAdd(&c->alg_flops, flops);
 }
 
 // ------------------------------------------------------------------ helpers
@@ -669,14 +673,43 @@ static int enqueue_bicgstab(sg_problem* P, bool graph, const Conds& cd, const do
     GridTab gt;
     gt.ng = t.nseg;
     for (int i = 0; i < t.nseg; ++i) gt.dof[i] = (double)(offs[i + 1] - offs[i]);
+    // all grids' applies of one half-iteration: serial on P->stream, or (small configurations)
+    // forked onto one stream per grid with private workspaces and joined again
+    auto applies = [&](const double* in, double* out) -> int {
+        if (!P->par_applies) {
+            for (size_t i = 0; i < gr.size(); ++i)
+                SG_TRY(apply_diag(P, *gr[i], in + offs[i], out + offs[i], P->scal + i * NSC + 5));
+            return SG_OK;
+        }
+        cudaStream_t main = P->stream;
+        double* ws0 = P->wsZ;
+        const size_t wsn0 = P->wsZ_n;
+        SG_CUDA(cudaEventRecord(P->ev_fork, main));
+        int rc = SG_OK;
+        for (size_t i = 0; i < gr.size() && rc == SG_OK; ++i) {
+            SG_CUDA(cudaStreamWaitEvent(P->par_streams[i], P->ev_fork, 0));
+            P->stream = P->par_streams[i];
+            P->wsZ = P->par_ws[i];
+            P->wsZ_n = P->par_ws_n[i];
+            P->stamp_slot = (int)i;
+            rc = apply_diag(P, *gr[i], in + offs[i], out + offs[i], P->scal + i * NSC + 5);
+            if (rc == SG_OK && cudaEventRecord(P->ev_join[i], P->par_streams[i]) != cudaSuccess) rc = SG_ERR_CUDA;
+        }
+        P->stream = main;
+        P->stamp_slot = 63;
+        P->wsZ = ws0;
+        P->wsZ_n = wsn0;
+        SG_TRY(rc);
+        for (size_t i = 0; i < gr.size(); ++i) SG_CUDA(cudaStreamWaitEvent(main, P->ev_join[i], 0));
+        return SG_OK;
+    };
     auto body = [&]() -> int {
         // v = A D^{-1} p
         if (!fuse) {
             k_seg_precond<<<nblk, 256, 0, P->stream>>>(t, S, P->scal, P->dinv, p, ph);
             P->launches++;
         }
-        for (size_t i = 0; i < gr.size(); ++i)
-            SG_TRY(apply_diag(P, *gr[i], ph + offs[i], v + offs[i], P->scal + i * NSC + 5));
+        SG_TRY(applies(ph, v));
         k_seg_dot<1><<<nblk, 256, 0, P->stream>>>(t, r0, v, nullptr, nullptr, P->red, nullptr, nullptr, P->scal);
         k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 1, P->red, P->scal, 6, 6, 1, tol2);
         P->launches += 2;
@@ -689,8 +722,7 @@ static int enqueue_bicgstab(sg_problem* P, bool graph, const Conds& cd, const do
             P->launches += 2;
         }
         // t = A D^{-1} s
-        for (size_t i = 0; i < gr.size(); ++i)
-            SG_TRY(apply_diag(P, *gr[i], sh + offs[i], tt + offs[i], P->scal + i * NSC + 5));
+        SG_TRY(applies(sh, tt));
         k_seg_dot<3><<<nblk, 256, 0, P->stream>>>(t, tt, s, tt, tt, P->red, s, s, P->scal);
         k_seg_finalize<<<t.nseg, 256, 0, P->stream>>>(t, 3, P->red, P->scal, 7, 8, 2, tol2);
         k_bicg_xr<<<nblk, 256, 0, P->stream>>>(t, P->scal, x, r, ph, sh, s, tt, r0, P->red);
@@ -877,6 +909,39 @@ int solver_init(sg_problem* P) {
     SG_CUDA(cudaMemset(P->ctl, 0, sizeof(SolveCtl)));
     SG_CUDA(cudaMallocHost(&P->hctl, sizeof(SolveCtl)));
     std::memset(P->hctl, 0, sizeof(SolveCtl));
+    // Concurrent per-grid applies when the configuration is launch-latency bound (every grid
+    // small) and the private intermediates fit: d = 1 only, whose pass kernels read no
+    // per-level constant-bank tables (the TMA / whole-x kernels of d >= 2 stage theirs in the
+    // module's constant bank and must stay serialised on one stream).
+    std::vector<const Grid*> gr;
+    for (auto& g : P->active) gr.push_back(&g);
+    for (auto& g : P->coarse) gr.push_back(&g);
+    size_t tot = 0, gmax = 0;
+    const size_t nb = std::max<size_t>(P->vorder.size(), 1);
+    for (auto* g : gr) {
+        const size_t w = nb * P->S * (size_t)g->n1 * (size_t)(g->n2 + (g->n2 & 1));
+        tot += w;
+        gmax = std::max<size_t>(gmax, (size_t)g->n1 * g->n2);
+    }
+    P->par_applies = P->fx.d == 1 && P->fv.d == 1 && getenv("SG_SERIAL_APPLIES") == nullptr &&
+                     gmax <= ((size_t)1 << 20) && tot * sizeof(double) <= ((size_t)1 << 30);
+    if (P->par_applies) {
+        SG_CUDA(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
+        for (auto* g : gr) {
+            cudaStream_t s;
+            cudaEvent_t e;
+            double* w;
+            const size_t n = nb * P->S * (size_t)g->n1 * (size_t)(g->n2 + (g->n2 & 1));
+            SG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            SG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            SG_CUDA(cudaMalloc(&w, sizeof(double) * n));
+            SG_CUDA(cudaMemset(w, 0, sizeof(double) * n));
+            P->par_streams.push_back(s);
+            P->ev_join.push_back(e);
+            P->par_ws.push_back(w);
+            P->par_ws_n.push_back(n);
+        }
+    }
     return SG_OK;
 }
 
@@ -885,6 +950,13 @@ int solver_destroy(sg_problem* P) {
     P->solve_graphs.clear();
     for (auto s : P->cap_streams) cudaStreamDestroy(s);
     P->cap_streams.clear();
+    for (auto s : P->par_streams) cudaStreamDestroy(s);
+    for (auto e : P->ev_join) cudaEventDestroy(e);
+    for (auto w : P->par_ws) cudaFree(w);
+    if (P->ev_fork) cudaEventDestroy(P->ev_fork);
+    P->par_streams.clear();
+    P->ev_join.clear();
+    P->par_ws.clear();
     cudaFree(P->ctl);
     if (P->hctl) cudaFreeHost(P->hctl);
     P->ctl = nullptr;

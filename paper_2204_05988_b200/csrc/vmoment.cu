@@ -29,40 +29,9 @@
 #include <cstring>
 
 #include "sg_internal.cuh"
+#include "vmom.cuh"
 
 namespace sg {
-
-namespace vm {
-// NPOLY monomial slots [1, y0, y1, y2, y0y0, y0y1, y0y2, y1y1, y1y2, y2y2]
-__host__ __device__ constexpr int mono_ax(int n, int which) {   // axes of monomial n (-1 none)
-    return n == 0 ? -1
-         : n <= 3 ? (which == 0 ? n - 1 : -1)
-         : n == 4 ? 0 : n == 5 ? (which == 0 ? 0 : 1) : n == 6 ? (which == 0 ? 0 : 2)
-         : n == 7 ? 1 : n == 8 ? (which == 0 ? 1 : 2) : 2;
-}
-__host__ __device__ constexpr int mono_deg(int n) { return n == 0 ? 0 : (n <= 3 ? 1 : 2); }
-__host__ __device__ constexpr int lin(int i) { return 1 + i; }
-__host__ __device__ constexpr int quad(int i, int j) {
-    return i > j ? quad(j, i) : (i == 0 ? 4 + j : (i == 1 ? 6 + j : 9));
-}
-__host__ __device__ constexpr bool mono_in(int D, int n) {   // monomial uses only axes < D
-    return mono_deg(n) == 0 || (mono_ax(n, 0) < D && (mono_deg(n) == 1 || mono_ax(n, 1) < D));
-}
-}  // namespace vm
-
-constexpr int VM_NP = 10;
-constexpr int VM_NC = 6;   // inflow (chi-weighted) groups
-struct VmOut {
-    double* p[VM_NP];   // output (group buffer) per monomial slot, nullptr if absent
-    double* pc[VM_NC];  // outputs of the chi-weighted groups (x-boundary rows only)
-};
-struct VmCoef {
-    double R[VM_NP][15];   // interior-class shifted-moment stencils
-    double H[VM_NC][15];   // interior-class half stencils of the chi groups (rows on the plane y_i = 0)
-    int off[15];           // lattice offsets of the Kuhn stencil
-    int nchi;
-    int chax[VM_NC], chkeep[VM_NC];   // chi group: weight y_i chi(keep * y_i > 0)
-};
 
 template <int D>
 __device__ __forceinline__ void vm_combine(const double (&zr)[VM_NP], const double* y, const VmOut& o, long long idx) {
@@ -455,6 +424,24 @@ int prepare_vmom(sg_problem* P) {
     return SG_OK;
 }
 
+// interior-class moment stencils, chi-group descriptors, lattice offsets and coordinates of v-level l2
+void vmom_coef(const sg_problem* P, int l2, VmCoef* cf, double* lo, double* h) {
+    const Factor& f = P->fv;
+    const Level& L = f.lev[l2];
+    std::memcpy(cf->R, P->vm_int[l2].data(), sizeof(cf->R));
+    std::memcpy(cf->H, P->vm_int[l2].data() + VM_NP * 15, sizeof(cf->H));
+    cf->nchi = P->vm_nchi;
+    for (int c = 0; c < VM_NC; ++c) {
+        cf->chax[c] = c < cf->nchi ? P->vm_chax[c] : 0;
+        cf->chkeep[c] = c < cf->nchi ? P->vm_chkeep[c] : 0;
+    }
+    for (int k = 0; k < 15; ++k) cf->off[k] = (int)L.so.off[k];
+    for (int q = 0; q < 3; ++q) {
+        lo[q] = q < f.d ? f.lo[q] : 0.0;
+        h[q] = q < f.d ? (f.hi[q] - f.lo[q]) / (L.m - 1) : 0.0;
+    }
+}
+
 // Z_g for the interior v-groups of grid (l1, l2) by moments; SG_ERR_UNSUPPORTED if unavailable
 int launch_vmom(sg_problem* P, int l2, int64_t nrows, int64_t n2, int64_t pitch, const double* X,
                 double* const* outs, const uint8_t* xflag, int64_t n1x) {
@@ -467,20 +454,9 @@ int launch_vmom(sg_problem* P, int l2, int64_t nrows, int64_t n2, int64_t pitch,
     for (int n = 0; n < VM_NP; ++n) o.p[n] = nullptr;
     for (int g = 0; g < P->ng_int; ++g) o.p[P->vm_slot[g]] = outs[g];
     VmCoef cf;
-    std::memcpy(cf.R, P->vm_int[l2].data(), sizeof(cf.R));
-    std::memcpy(cf.H, P->vm_int[l2].data() + VM_NP * 15, sizeof(cf.H));
-    cf.nchi = P->vm_nchi;
-    for (int c = 0; c < VM_NC; ++c) {
-        cf.chax[c] = c < cf.nchi ? P->vm_chax[c] : 0;
-        cf.chkeep[c] = c < cf.nchi ? P->vm_chkeep[c] : 0;
-        o.pc[c] = c < cf.nchi ? outs[P->ng_int + c] : nullptr;
-    }
-    for (int k = 0; k < 15; ++k) cf.off[k] = (int)L.so.off[k];
-    double lo[3] = {0, 0, 0}, h[3] = {0, 0, 0};
-    for (int q = 0; q < d; ++q) {
-        lo[q] = f.lo[q];
-        h[q] = (f.hi[q] - f.lo[q]) / (m - 1);
-    }
+    double lo[3], h[3];
+    vmom_coef(P, l2, &cf, lo, h);
+    for (int c = 0; c < VM_NC; ++c) o.pc[c] = c < cf.nchi ? outs[P->ng_int + c] : nullptr;
     const int W = f.W;
     // threads = columns x row blocks (VR rows each), about 16 resident warps per SM
     const long long target = 148LL * 2048;

@@ -23,10 +23,13 @@
 // kernel parameters (constant-bank operands of DFMA, no loads); near the
 // boundary they are read from the class table tab[cls][g][k] with warp-uniform
 // addresses (broadcast), and the boundary-only (face) groups are included.
+#include <array>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "sg_internal.cuh"
+#include "vmom.cuh"
 
 namespace sg {
 namespace xfi {
@@ -521,4 +524,327 @@ int launch_xwhole(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pitch, 
     SG_CUDA(cudaGetLastError());
     return SG_OK;
 }
+}  // namespace sg
+
+namespace sg {
+// =====================================================================
+// Fused single-pass strip operator on grids with a tiny x factor (level-1 x-lattice of
+// m^d <= 27 rows; d = 2 also m = 5): the two-sided apply
+//     Y[r][a] = sum_g sum_k C_g[r, r + off_k] Z_g[r + off_k][a],   Z_g = (Id x B_g) X
+// (application order l.516-532) without intermediates in memory.
+// One thread owns one v-column a and ALL x-rows: for every source x-row r it loads the W
+// v-neighbours X[r][a + off_k] (L1/L2), forms the shifted-moment sums ZR_m (vmoment.cu:
+// compile-time kernel-parameter coefficients when the whole warp is interior, the shared-
+// memory class table otherwise), combines them into Z_g for every interior monomial group
+// and the chi-weighted inflow groups (x-boundary rows only), and scatters Z_g into the
+// register accumulators of the x-rows whose stencil contains r.  The x coefficients are
+// the per-row class values of the combined matrices C_g in the constant bank, laid out in
+// the kernel's visiting order (source row, group, target, offset) so every address is a
+// compile-time constant.  X is read once (its v-halo from cache), Y written once.
+// =====================================================================
+constexpr int FW_NG = VM_NP + VM_NC;
+static_assert(FW_NG <= XW_MAXG, "fused whole-x table shares the whole-x constant bank");
+#define c_fw c_xw   // [g][pair in (source, target, offset) order]; staged before every launch
+
+namespace fw {
+// compile-time pair lists: for source row R the (target, offset) pairs with nbr(target, offset) = R
+struct PairList {
+    int n;
+    int t[15];
+};
+template <int D, int M>
+__host__ __device__ constexpr PairList make_pairs(int R) {
+    PairList p{0, {0}};
+    constexpr int N = D == 3 ? M * M * M : M * M;
+    constexpr int W = D == 3 ? 15 : 7;
+    for (int t = 0; t < N; ++t)
+        for (int k = 0; k < W; ++k)
+            if (xw::nbr<D, M>(t, k) == R) p.t[p.n++] = t;
+    return p;
+}
+template <int D, int M>
+__host__ __device__ constexpr int pair_base(int R) {   // pairs of the source rows before R
+    int c = 0;
+    for (int r = 0; r < R; ++r) c += make_pairs<D, M>(r).n;
+    return c;
+}
+template <int D, int M, int R>
+struct Row {
+    static constexpr PairList p = make_pairs<D, M>(R);
+    static constexpr int base = pair_base<D, M>(R);
+    static constexpr bool xbnd = [] {
+        int zz = R;
+        bool b = false;
+        for (int q = 0; q < D; ++q) {
+            const int zq = zz % M;
+            zz /= M;
+            b = b || zq == 0 || zq == M - 1;
+        }
+        return b;
+    }();
+};
+// acc[t_j] += c[j] * z for the compile-time pairs j of source row R
+template <int D, int M, int R, int J>
+struct Scatter {
+    template <int N>
+    __device__ __forceinline__ static void run(double (&acc)[N], const double* c, double z) {
+        if constexpr (J < Row<D, M, R>::p.n) {
+            constexpr int t = Row<D, M, R>::p.t[J];
+            acc[t] = fma(c[J], z, acc[t]);
+            Scatter<D, M, R, J + 1>::run(acc, c, z);
+        }
+    }
+};
+}  // namespace fw
+
+struct FwCtx {                 // per-thread state of the fused whole-x kernel
+    const double* x;           // X + column
+    int n2;
+    unsigned nbmask;           // bit k: neighbour a + off_k inside the v-lattice
+    bool warp_int;             // every column of the warp is interior (d = 2 path)
+    const double* ct;          // class row of the moment table (shared memory)
+    double y[3];
+};
+
+template <int D, int M, int NP, int R>
+__device__ __forceinline__ void fw_row(double (&acc)[D == 3 ? M * M * M : M * M], const FwCtx& cx, const VmCoef& cf) {
+    constexpr int N = D == 3 ? M * M * M : M * M;
+    constexpr int W = D == 3 ? 15 : 7;
+    if constexpr (R < N) {
+        const double* xr = cx.x + (long long)R * cx.n2;
+        // moment sums.  d = 3: class-table row of the column (shared memory, one broadcast address
+        // for the interior columns) in a rolled offset loop, which keeps the 27 unrolled source rows
+        // small enough for the instruction cache (measured 5.89 -> 5.12 ms on configs[4] grid (1,7));
+        // d = 2: fully unrolled, compile-time kernel-parameter coefficients for interior warps
+        // (measured faster there: grid (1,11) of configs[2] 1.00 -> 0.81 ms)
+        double zr[VM_NP];
+#pragma unroll
+        for (int n = 0; n < VM_NP; ++n) zr[n] = 0.0;
+        if constexpr (D == 3) {
+#pragma unroll 5
+            for (int k = 0; k < W; ++k) {
+                const double xk = (cx.nbmask >> k) & 1u ? __ldg(xr + cf.off[k]) : 0.0;
+#pragma unroll
+                for (int n = 0; n < VM_NP; ++n)
+                    if (vm::mono_in(D, n)) zr[n] = fma(cx.ct[n * W + k], xk, zr[n]);
+            }
+        } else {
+            double xv[W];
+#pragma unroll
+            for (int k = 0; k < W; ++k) xv[k] = (cx.nbmask >> k) & 1u ? __ldg(xr + cf.off[k]) : 0.0;
+            if (cx.warp_int) {
+#pragma unroll
+                for (int n = 0; n < VM_NP; ++n)
+                    if (vm::mono_in(D, n))
+#pragma unroll
+                        for (int k = 0; k < W; ++k) zr[n] = fma(cf.R[n][k], xv[k], zr[n]);
+            } else {
+#pragma unroll
+                for (int n = 0; n < VM_NP; ++n)
+                    if (vm::mono_in(D, n))
+#pragma unroll
+                        for (int k = 0; k < W; ++k) zr[n] = fma(cx.ct[n * W + k], xv[k], zr[n]);
+            }
+        }
+        constexpr int base = fw::Row<D, M, R>::base;
+        const double* y = cx.y;
+#pragma unroll
+        for (int g = 0; g < VM_NP; ++g) {
+            if (!vm::mono_in(D, g)) continue;
+            double zg;
+            if (g == 0) {
+                zg = zr[0];
+            } else if (g <= 3) {
+                zg = fma(y[g - 1], zr[0], zr[g]);
+            } else {
+                const int i = vm::mono_ax(g, 0), j = vm::mono_ax(g, 1);
+                if (i == j)
+                    zg = fma(y[i] * y[i], zr[0], fma(2.0 * y[i], zr[vm::lin(i)], zr[g]));
+                else
+                    zg = fma(y[i] * y[j], zr[0], fma(y[i], zr[vm::lin(j)], fma(y[j], zr[vm::lin(i)], zr[g])));
+            }
+            fw::Scatter<D, M, R, 0>::run(acc, c_xw + g * NP + base, zg);
+        }
+        if constexpr (fw::Row<D, M, R>::xbnd) {   // chi-weighted inflow groups (x-boundary rows)
+#pragma unroll 1
+            for (int c = 0; c < cf.nchi; ++c) {
+                const int i = cf.chax[c];
+                const double yi = i == 0 ? y[0] : (i == 1 ? y[1] : y[2]);
+                const double zi = i == 0 ? zr[1] : (i == 1 ? zr[2] : zr[3]);
+                double zg = cf.chkeep[c] * yi > 0.0 ? fma(yi, zr[0], zi) : 0.0;
+                if (yi == 0.0) {   // column on the plane y_i = 0: half stencil (X reloaded, rare)
+                    zg = 0.0;
+                    const double* hc = cx.ct + (VM_NP + c) * W;
+                    for (int k = 0; k < W; ++k)
+                        if ((cx.nbmask >> k) & 1u) zg = fma(hc[k], __ldg(xr + cf.off[k]), zg);
+                }
+                fw::Scatter<D, M, R, 0>::run(acc, c_xw + (VM_NP + c) * NP + base, zg);
+            }
+        }
+        fw_row<D, M, NP, R + 1>(acc, cx, cf);
+    }
+}
+
+template <int D, int M>
+__global__ void __launch_bounds__(128) k_fwhole(const double* __restrict__ X, double* __restrict__ Y, int n2, int mv,
+                                                const double* __restrict__ tab, const __grid_constant__ VmCoef cf,
+                                                double lo0, double lo1, double lo2, double h0, double h1, double h2,
+                                                const double* __restrict__ skip) {
+    if (skip && *skip != 0.0) return;   // grid converged (batched block solver)
+    constexpr int N = D == 3 ? M * M * M : M * M;
+    constexpr int W = D == 3 ? 15 : 7;
+    constexpr int NP = fw::pair_base<D, M>(N);
+    constexpr int NC = D == 3 ? 27 : 9;
+    constexpr int NR = VM_NP + VM_NC;
+    constexpr int CS = NR * W + 1;
+    constexpr int ICLS = D == 3 ? 13 : 4;
+    extern __shared__ double st[];   // [NC][CS] moment class table
+    for (int i = threadIdx.x; i < NC * NR * W; i += blockDim.x) {
+        const int c = i / (NR * W);
+        st[c * CS + (i - c * NR * W)] = tab[i];
+    }
+    __syncthreads();
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = a < n2;
+    const int ac = valid ? a : n2 - 1;
+    const int z[3] = {ac % mv, (ac / mv) % mv, D == 3 ? ac / (mv * mv) : 0};
+    int cls = 0, mul = 1;
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+        cls += mul * (z[q] == 0 ? 0 : (z[q] == mv - 1 ? 2 : 1));
+        mul *= 3;
+    }
+    FwCtx cx;
+    cx.x = X + ac;
+    cx.n2 = n2;
+    cx.warp_int = __all_sync(0xffffffffu, cls == ICLS);
+    cx.ct = st + cls * CS;
+    cx.y[0] = lo0 + h0 * z[0];
+    cx.y[1] = lo1 + h1 * z[1];
+    cx.y[2] = lo2 + h2 * z[2];
+    cx.nbmask = 0;
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        const int c = ac + cf.off[k];
+        cx.nbmask |= (c >= 0 && c < n2) ? (1u << k) : 0u;   // (absent neighbours have zero coefficients)
+    }
+    double acc[N];
+#pragma unroll
+    for (int r = 0; r < N; ++r) acc[r] = 0.0;
+    fw_row<D, M, NP, 0>(acc, cx, cf);
+    if (!valid) return;
+#pragma unroll
+    for (int r = 0; r < N; ++r) Y[(long long)r * n2 + a] = acc[r];
+}
+
+// [g][pair] tables of the fused whole-x kernel (setup time, after prepare_vmom): group slot
+// g < VM_NP is the interior group of monomial g, g >= VM_NP the chi group g - VM_NP (vorder);
+// pairs in the kernel's visiting order (source row r, target t, offset k with nbr(t,k) = r).
+int prepare_fwhole(sg_problem* P) {
+    P->fw_dev.assign(P->F + 1, nullptr);
+    const int d = P->fx.d, W = P->fx.W;
+    const int nga = (int)P->vorder.size();
+    if (P->fx.kind != SG_MESH_BOX || P->fv.kind != SG_MESH_BOX || P->S != 1 || d < 2) return SG_OK;
+    if (P->vm_nchi != nga - P->ng_int || P->ng_int > VM_NP) return SG_OK;
+    int slot_group[FW_NG];
+    for (int g = 0; g < FW_NG; ++g) slot_group[g] = -1;
+    for (int o = 0; o < P->ng_int; ++o) {
+        if (P->vm_slot[o] < 0) return SG_OK;
+        slot_group[P->vm_slot[o]] = o;
+    }
+    for (int c = 0; c < P->vm_nchi; ++c) slot_group[VM_NP + c] = P->ng_int + c;
+    for (int l1 = 1; l1 <= P->F && l1 < (int)P->xfi_tab.size(); ++l1) {
+        if (!P->xfi_tab[l1]) continue;
+        const int m = P->fx.lev[l1].m;
+        const bool ok = (d == 3 && m == 3) || (d == 2 && (m == 3 || m == 5));
+        if (!ok) continue;
+        const int64_t n1 = P->fx.lev[l1].n;
+        int ncls = 1;
+        for (int q = 0; q < d; ++q) ncls *= 3;
+        std::vector<double> cls((size_t)ncls * nga * W);
+        SG_CUDA(cudaMemcpy(cls.data(), P->xfi_tab[l1], sizeof(double) * cls.size(), cudaMemcpyDeviceToHost));
+        auto lat = [&](int r, int* zz) {
+            for (int q = 0; q < d; ++q) {
+                zz[q] = r % m;
+                r /= m;
+            }
+        };
+        auto nbr = [&](int t, int k) {
+            int zz[3] = {0, 0, 0};
+            lat(t, zz);
+            int out = 0, mul = 1;
+            for (int q = 0; q < d; ++q) {
+                const int dq = d == 3 ? (q == 0 ? xfi::d0_3(k) : q == 1 ? xfi::d1_3(k) : xfi::d2_3(k))
+                                      : (q == 0 ? xfi::d0_2(k) : xfi::d1_2(k));
+                const int v = zz[q] + dq;
+                if (v < 0 || v >= m) return -1;
+                out += mul * v;
+                mul *= m;
+            }
+            return out;
+        };
+        std::vector<std::array<int, 2>> pairs;   // (target, offset) in visiting order
+        for (int r = 0; r < n1; ++r)
+            for (int t = 0; t < n1; ++t)
+                for (int k = 0; k < W; ++k)
+                    if (nbr(t, k) == r) pairs.push_back({t, k});
+        const int np = (int)pairs.size();
+        if (np > XW_MAXP) continue;
+        std::vector<double> tab((size_t)FW_NG * np, 0.0);
+        for (int g = 0; g < FW_NG; ++g) {
+            const int o = slot_group[g];
+            if (o < 0) continue;
+            for (int j = 0; j < np; ++j) {
+                const int t = pairs[j][0], k = pairs[j][1];
+                int zz[3] = {0, 0, 0};
+                lat(t, zz);
+                int c = 0, mul = 1;
+                for (int q = 0; q < d; ++q) {
+                    c += mul * (zz[q] == 0 ? 0 : (zz[q] == m - 1 ? 2 : 1));
+                    mul *= 3;
+                }
+                tab[(size_t)g * np + j] = cls[((size_t)c * nga + o) * W + k];
+            }
+        }
+        SG_CUDA(cudaMalloc(&P->fw_dev[l1], sizeof(double) * tab.size()));
+        SG_CUDA(cudaMemcpy(P->fw_dev[l1], tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice));
+        P->fw_np = np;
+    }
+    return SG_OK;
+}
+
+// the whole strip-operator apply of grid (l1, l2) in one fused launch; SG_ERR_UNSUPPORTED if the
+// grid is not covered (x-lattice not tiny, moment tables unavailable, S = 2, ...)
+int launch_fwhole(sg_problem* P, int l1, int l2, int64_t n2, const double* X, double* Y) {
+    if (!P->use_fused || l1 >= (int)P->fw_dev.size() || !P->fw_dev[l1]) return SG_ERR_UNSUPPORTED;
+    if (l2 >= (int)P->vm_ok.size() || !P->vm_ok[l2] || !P->vm_tab[l2]) return SG_ERR_UNSUPPORTED;
+    const int d = P->fx.d, m = P->fx.lev[l1].m;
+    const int n1 = (int)P->fx.lev[l1].n;
+    if ((int64_t)n1 * n2 >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
+    VmCoef cf;
+    double lo[3], h[3];
+    vmom_coef(P, l2, &cf, lo, h);
+    const int np = d == 3 ? 223 : (m == 3 ? 41 : 137);
+    SG_CUDA(cudaMemcpyToSymbolAsync(c_fw, P->fw_dev[l1], sizeof(double) * FW_NG * np, 0, cudaMemcpyDeviceToDevice,
+                                    P->stream));
+    const int W = P->fv.W;
+    const int smb = (d == 3 ? 27 : 9) * ((VM_NP + VM_NC) * W + 1) * (int)sizeof(double);
+    const unsigned blocks = (unsigned)((n2 + 127) / 128);
+    const int mv = P->fv.lev[l2].m;
+#define FWL(DD, MM)                                                                                              \
+    do {                                                                                                         \
+        cudaFuncSetAttribute(k_fwhole<DD, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb);                \
+        k_fwhole<DD, MM><<<blocks, 128, smb, P->stream>>>(X, Y, (int)n2, mv, P->vm_tab[l2], cf, lo[0], lo[1],   \
+                                                           lo[2], h[0], h[1], h[2], P->skip);                    \
+    } while (0)
+    if (d == 3 && m == 3) FWL(3, 3);
+    else if (d == 2 && m == 3) FWL(2, 3);
+    else if (d == 2 && m == 5) FWL(2, 5);
+    else return SG_ERR_UNSUPPORTED;
+#undef FWL
+    P->launches++;
+    SG_CUDA(cudaGetLastError());
+    return SG_OK;
+}
+
 }  // namespace sg

@@ -295,10 +295,11 @@ def test_zero_rhs_gives_zero():
     assert it == 1 and float(u.abs().max()) == 0.0
 
 
-@pytest.mark.parametrize("env", ["SG_NO_TMA"])
+@pytest.mark.parametrize("env", ["SG_NO_TMA", "SG_NO_FUSED"])
 @pytest.mark.parametrize("name", CONFIG_ORDER)
 def test_apply_strip_operator_kernel_paths(name, env, monkeypatch):
-    """Same parity on the fallback of the TMA line sweep (register line sweep k_xfanin)."""
+    """Same parity on the fallbacks: of the TMA line sweep (register line sweep k_xfanin) and
+    of the fused whole-x apply (moment pass 1 + whole-x pass 2)."""
     from oracle.sgrid import SGProblem
     from paper_2204_05988_b200 import Problem
     key, _, val = env.partition("=")
@@ -346,6 +347,26 @@ def test_apply_strip_operator_full_size():
     g.sg_apply_strip_operator(SET_ACTIVE, gi, torch.from_numpy(X.ravel()).cuda(), Yt)
     ref = o.apply_pair(o.terms, (4, 4), (4, 4), X)
     assert relmax(Yt.cpu().numpy().reshape(X.shape), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("name,L", [("c2_4d_stream", 8), ("c4_6d_stream", 5)])
+def test_apply_strip_operator_fused_sizes(name, L):
+    """Every active and coarse grid at a level where the fused whole-x kernel engages on many
+    column blocks with a ragged tail (configs[2] L = 8: level-1/2 x-lattices (1,7), (2,6), ...;
+    configs[4] L = 5: (1,4), (1,3)) next to the two-pass kernels of the other grids, element by
+    element against the oracle (factors assembled on each grid's own levels)."""
+    from oracle.problem import delta_hmin, strip_terms
+    from oracle.sgrid import SGProblem
+    from paper_2204_05988_b200 import Problem
+    cfg = get_config(name, L=L)
+    g, o = Problem(cfg), SGProblem(cfg, galerkin="direct")
+    rng = np.random.default_rng(31)
+    for set_, grids in ((SET_ACTIVE, o.active), (SET_COARSE, o.coarse)):
+        for gi, l in enumerate(grids):
+            X = rng.standard_normal(o.shape(l))
+            Yt = torch.empty(X.size, dtype=torch.float64, device="cuda")
+            g.sg_apply_strip_operator(set_, gi, torch.from_numpy(X.ravel()).cuda(), Yt)
+            assert relmax(Yt.cpu().numpy().reshape(X.shape), o.apply_diag(l, X)) <= 1e-12, (set_, l)
 
 
 def _sample_nodes(m, d, n_random, rng):
@@ -407,8 +428,11 @@ def test_apply_strip_operator_full_size_c3():
 
 def test_full_size_c1_every_grid_and_one_strip():
     """configs[1] at its full size (L=14, 491 K active DOF, dG(1)): the strip operator on every
-    active and coarse grid element by element, and one strip (rhs from the interpolated u0,
-    the strip solve, the trace) against the oracle's direct-LU Richardson at rtol 1e-13."""
+    active and coarse grid element by element; the first strip's right-hand side (interpolated
+    u0, jump load) element by element; and the GPU strip solution (rtol 1e-13) checked by a
+    property that holds at any size: it solves the Galerkin system A^(delta) U = b of the strip
+    (PAPER.md l.424-438), its residual evaluated with the ORACLE's cross-grid operator
+    E^T A_F E (one oracle apply, ~1.5 min; the oracle's own direct-LU Richardson needs hours)."""
     from oracle.sgrid import SGProblem
     from paper_2204_05988_b200 import Problem
     cfg = get_config("c1_2d_rot")
@@ -420,11 +444,22 @@ def test_full_size_c1_every_grid_and_one_strip():
             Yt = torch.empty(X.size, dtype=torch.float64, device="cuda")
             g.sg_apply_strip_operator(set_, gi, torch.from_numpy(X.ravel()).cuda(), Yt)
             assert relmax(Yt.cpu().numpy().reshape(X.shape), o.apply_diag(l, X)) <= 1e-12, (set_, l)
-    tr_ref, _, _ = o.run(nsteps=1, rtol=1e-13)
+    tr0 = o.interp_u0()
+    b_ref = o.rhs(1, tr0)
     u0 = torch.zeros(g.set_size(SET_ACTIVE, 1), dtype=torch.float64, device="cuda")
     g.sg_interp_u0(u0)
-    g.sg_step(1, 1, u0, rtol=1e-13, inner_rtol=1e-13)
-    assert relmax(_full(o, to_blocks(g, u0, S=1)), _full(o, tr_ref)) <= 1e-9
+    bt = torch.zeros(g.set_size(SET_ACTIVE, o.S), dtype=torch.float64, device="cuda")
+    g.sg_rhs(1, u0, bt)
+    gb = to_blocks(g, bt)
+    for l in o.active:
+        assert relmax(gb[l], b_ref[l]) <= 1e-12, l
+    ut = torch.zeros_like(bt)
+    g.sg_solve_strip(bt, ut, rtol=1e-13, inner_rtol=1e-13, max_iter=200)
+    U = to_blocks(g, ut)
+    AU = o.apply_full(o.terms, U)
+    nb = max(np.abs(b_ref[l]).max() for l in o.active)
+    res = max(np.abs(AU[l] - b_ref[l]).max() for l in o.active)
+    assert res <= 1e-9 * nb, res / nb
 
 
 def test_apply_strip_operator_full_size_4d():

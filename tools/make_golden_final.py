@@ -6,7 +6,6 @@ input module sginputs/ (no CUDA path).
 
   python tools/make_golden_final.py c0_2d_const 6
   python tools/make_golden_final.py c1_2d_rot 5
-  python tools/make_golden_final.py c1_2d_rot 14 1     # first strip only (full-size configs[1])
 """
 import os
 import sys
