@@ -782,7 +782,9 @@ static int apply_cross_impl(sg_problem* P, const double* Tb, int S_out, int S_in
     // an independent branch (own stream, chain and Horner workspaces, partial output), summed at
     // the end; otherwise all groups run serially on the handle's stream into Y.
     const int nxg_all = ng >= 2 ? (mass ? 1 : (int)P->xgroups.size()) : 0;
-    const bool par = P->par_cross && !lower_done && nvg + nxg_all <= (int)P->cx_streams.size() &&
+    // (not inside the strip-solve graph: forking these streams there crashed the driver in
+    //  cuStreamEndCapture on the box's driver 580.159, profiles/r2d/dbg_gdb.log)
+    const bool par = P->par_cross && !P->capturing && !lower_done && nvg + nxg_all <= (int)P->cx_streams.size() &&
                      (int64_t)set_size(P, SG_SET_ACTIVE, S_out) <= P->cx_y_n &&
                      (int64_t)set_size(P, SG_SET_ACTIVE, S_in) * 2 <= P->cx_h_n;
     cudaStream_t main_stream = P->stream;
