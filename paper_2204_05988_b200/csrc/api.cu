@@ -58,6 +58,9 @@ extern "C" int sg_create(const sg_config* cfg, void* stream, sg_problem** out) {
     P->use_tma = getenv("SG_NO_TMA") == nullptr;
     // fused whole-x apply on the tiny x-lattices (fallback: moment pass 1 + whole-x pass 2)
     P->use_fused = getenv("SG_NO_FUSED") == nullptr;
+    // experiment knobs of the L2-resident chunked apply (MB of intermediates per chunk; 0 = off)
+    if (getenv("SG_L2_MB")) P->l2_chunk_bytes = (int64_t)(atof(getenv("SG_L2_MB")) * 1048576.0);
+    if (getenv("SG_L2_MINCOLS")) P->l2_chunk_mincols = atoi(getenv("SG_L2_MINCOLS"));
     // fallback of the batched cross-grid lower part (also taken when its buffers do not fit)
     P->use_cross_batched = getenv("SG_NO_CROSS_BATCH") == nullptr;
     // outer step length (reading R13): 0 Richardson + MR safeguard, 1 plain, 2 MR always
@@ -194,6 +197,7 @@ extern "C" int sg_assemble_factors(sg_problem* P) {
 static void free_level(Level& L) {
     cudaFree(L.lat); cudaFree(L.cols); cudaFree(L.pcols); cudaFree(L.pvals); cudaFree(L.rcols); cudaFree(L.rvals);
     cudaFree(L.bflag);
+    cudaFree(L.bmask);
     for (double* p : L.fm) cudaFree(p);
     for (double* p : L.fst) cudaFree(p);
     for (double* p : L.fcls) cudaFree(p);

@@ -369,42 +369,59 @@ template <int D, int R, int MINB = 2>
 __global__ void __launch_bounds__(VF_TC * VF_RL, MINB) k_vfan_st(int64_t nrows, int64_t n1, int64_t n2, StencilOff so,
                                                               const uint8_t* __restrict__ xflag, VfanParams vp,
                                                               const double* __restrict__ X, int64_t rows_per_block,
-                                                              int64_t opitch, const double* __restrict__ skip) {
+                                                              int64_t opitch, const double* __restrict__ skip,
+                                                              int64_t c0, int64_t c1, int maskmode) {
+    // columns [c0, c1) only (L2-resident column chunks); output column a - c0.
+    // xflag[row]: maskmode 0: non-zero on x-boundary rows (all boundary-only groups computed there);
+    // maskmode 1: bit j set when boundary-only group ng_int + j is needed on this row
     if (skip && *skip != 0.0) return;   // grid converged (batched block solver)
     constexpr int W = stc::Bands<D>::W;
     extern __shared__ double sm[];
     const int tx = threadIdx.x, ty = threadIdx.y;
-    const int64_t a = blockIdx.x * VF_TC + tx;
-    const bool aval = a < n2;
+    const int64_t a = c0 + blockIdx.x * VF_TC + tx;
+    const bool aval = a < c1;
     const int tot = vp.ng * W * VF_TC;
     for (int idx = ty * VF_TC + tx; idx < tot; idx += VF_TC * VF_RL) {
         const int g = idx / (W * VF_TC), rem = idx - g * W * VF_TC, k = rem / VF_TC, c = rem - k * VF_TC;
-        const int64_t ac = blockIdx.x * VF_TC + c;
-        sm[idx] = ac < n2 ? __ldg(vp.vst[g] + k * n2 + ac) : 0.0;
+        const int64_t ac = c0 + blockIdx.x * VF_TC + c;
+        sm[idx] = ac < c1 ? __ldg(vp.vst[g] + k * n2 + ac) : 0.0;
     }
     __syncthreads();
-    int32_t addr[W];   // column offsets within a row (n2 < 2^31)
+    // X is addressed as uniform base + 32-bit byte offset (nrows * n2 * 8 < 2^32 checked on the host):
+    // one integer add per load instead of a 64-bit address computation
+    uint32_t addr8[W];   // byte offsets of the stencil columns within a row
 #pragma unroll
     for (int k = 0; k < W; ++k) {
         int64_t c = a + so.off[k];
-        addr[k] = (int32_t)(c < 0 ? 0 : (c >= n2 ? n2 - 1 : c));
+        addr8[k] = (uint32_t)(c < 0 ? 0 : (c >= n2 ? n2 - 1 : c)) * 8u;
     }
-    const int64_t rb = blockIdx.y * rows_per_block;
-    const int64_t re = min(nrows, rb + rows_per_block);
-    for (int64_t r0 = rb + ty * R; r0 < re; r0 += VF_RL * R) {
+    const int rb = (int)(blockIdx.y * rows_per_block);
+    const int re = (int)min(nrows, (int64_t)rb + rows_per_block);
+    const int n1i = (int)n1;
+    const bool one_s = nrows == n1;
+    const uint32_t row8 = (uint32_t)n2 * 8u;
+    uint32_t xoff8 = (uint32_t)(rb + ty * R) * row8;
+    const uint32_t xstep8 = (uint32_t)(VF_RL * R) * row8;
+    int64_t ooff = (int64_t)(rb + ty * R) * opitch + (a - c0);
+    const int64_t ostep = (int64_t)VF_RL * R * opitch;
+    const char* Xb = reinterpret_cast<const char*>(X);
+    for (int r0 = rb + ty * R; r0 < re; r0 += VF_RL * R, xoff8 += xstep8, ooff += ostep) {
         double x[R][W];
-        bool anyb = false;
+        unsigned rm = 0;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int64_t row = r0 + r;
+            const int row = r0 + r;
             const bool ok = row < re && aval;
-            const double* base = X + (ok ? row : 0) * n2;
+            const uint32_t rbase = xoff8 + (uint32_t)r * row8;
 #pragma unroll
-            for (int k = 0; k < W; ++k) x[r][k] = ok ? __ldg(base + addr[k]) : 0.0;
-            if (row < re) anyb |= xflag[row % n1] != 0;
+            for (int k = 0; k < W; ++k)
+                x[r][k] = ok ? __ldg(reinterpret_cast<const double*>(Xb + (uint32_t)(rbase + addr8[k]))) : 0.0;
+            if (row < re) rm |= xflag[one_s ? row : row % n1i];
         }
-        const int ngu = anyb ? vp.ng : vp.ng_int;
+        const unsigned long long bneed = maskmode ? (unsigned long long)rm : (rm ? ~0ULL : 0ULL);
+        const int ngu = bneed ? vp.ng : vp.ng_int;
         for (int g = 0; g < ngu; ++g) {
+            if (g >= vp.ng_int && !((bneed >> (g - vp.ng_int)) & 1ULL)) continue;
             double acc[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) acc[r] = 0.0;
@@ -414,10 +431,10 @@ __global__ void __launch_bounds__(VF_TC * VF_RL, MINB) k_vfan_st(int64_t nrows, 
 #pragma unroll
                 for (int r = 0; r < R; ++r) acc[r] = fma(c, x[r][k], acc[r]);
             }
-            double* o = vp.out[g];
+            double* o = vp.out[g] + ooff;
 #pragma unroll
             for (int r = 0; r < R; ++r)
-                if (r0 + r < re && aval) o[(r0 + r) * opitch + a] = acc[r];
+                if (r0 + r < re && aval) o[r * opitch] = acc[r];
         }
     }
 }
@@ -828,11 +845,16 @@ int class_compress(sg_problem* P, const Factor& f, int l, const double* st, doub
 }
 
 int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, const uint8_t* xflag,
-                   const VfanParams& vp, const double* X, int64_t opitch) {
-    if (opitch <= 0) opitch = n2;
+                   const VfanParams& vp, const double* X, int64_t opitch, int64_t c0, int64_t c1, int maskmode) {
+    if (c1 <= 0) c1 = n2;
+    if (opitch <= 0) opitch = c1 - c0;
     const int W = (1 << (d + 1)) - 1;
     const int64_t nrows = (int64_t)S * n1;
-    const int64_t ctiles = (n2 + VF_TC - 1) / VF_TC;
+    const int64_t ctiles = (c1 - c0 + VF_TC - 1) / VF_TC;
+    if (nrows * n2 >= (1LL << 29)) {
+        set_error("k_vfan_st: grid too large for 32-bit byte offsets");
+        return SG_ERR_UNSUPPORTED;
+    }
     // enough blocks to fill the machine, as many rows per block as possible (coefficient reuse)
     constexpr int vf_mult = 12;   // blocks per SM, measured best in round 1
     int64_t rchunks = std::max<int64_t>(1, (148 * vf_mult + ctiles - 1) / ctiles);
@@ -843,14 +865,14 @@ int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const St
     dim3 grid((unsigned)ctiles, (unsigned)rchunks), block(VF_TC, VF_RL);
     if (d == 1) {
         cudaFuncSetAttribute(k_vfan_st<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_vfan_st<1, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch, P->skip);
+        k_vfan_st<1, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch, P->skip, c0, c1, maskmode);
     } else if (d == 2) {
         cudaFuncSetAttribute(k_vfan_st<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_vfan_st<2, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch, P->skip);
+        k_vfan_st<2, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch, P->skip, c0, c1, maskmode);
     } else {
         // R = 2 rows per thread (R = 3/4 measured 4-11 % slower in round 1: register-starved)
         cudaFuncSetAttribute(k_vfan_st<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_vfan_st<3, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch, P->skip);
+        k_vfan_st<3, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch, P->skip, c0, c1, maskmode);
     }
     P->launches++;
     SG_CUDA(cudaGetLastError());

@@ -68,6 +68,7 @@ struct Level {
     std::vector<double*> fst;   // per spec id: stencil format [W][n] (box lattices), nullptr if unused
     std::vector<double*> fcls;  // per spec id: class table [27][W] if translation invariant
     uint8_t* bflag = nullptr;   // 1 for lattice-boundary nodes
+    uint8_t* bmask = nullptr;   // x-levels: bit j set when boundary-only v-group j has this row in its face (null: use bflag)
     int64_t nbnd = 0;           // number of boundary nodes
     StencilOff so;              // stencil offsets (box lattices)
 };
@@ -280,6 +281,8 @@ struct sg_problem {
     std::vector<double*> xfi_tab;
     std::vector<double*> xfi_itab;
     std::vector<std::vector<double>> xfi_cint;
+    // ... and per boundary class the boundary-only (face) groups with a nonzero row or column there
+    std::vector<std::vector<uint8_t>> xfi_cmask;
     // whole-x pass 2 (tiny x-lattices), per x-level: compact [group][pair] coefficient table
     std::vector<double*> xw_tab;   // non-null when the whole-x tables exist
     std::vector<double*> xw_dev;
@@ -288,6 +291,9 @@ struct sg_problem {
     std::vector<double*> fw_dev;
     int fw_np = 0;
     bool use_fused = true;
+    // L2-resident column chunks of the two-pass apply: intermediates per chunk (bytes; 0 = off)
+    int64_t l2_chunk_bytes = 0;
+    int64_t l2_chunk_mincols = 64;
     // batched cross-grid lower part: stage-0 fan-outs of all v-groups and the Horner
     // results per target and group (even pitch); also used by the batched upper part
     double* cross_q = nullptr;
@@ -334,7 +340,8 @@ int launch_sum_into(sg_problem* P, int64_t n, int k, double* const* xs, double* 
 int launch_ell_to_stencil(sg_problem* P, int64_t n, int W, const int32_t* cols, const double* vals,
                           const StencilOff& so, double* out);
 int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const StencilOff& so, const uint8_t* xflag,
-                   const VfanParams& vp, const double* X, int64_t opitch = 0);
+                   const VfanParams& vp, const double* X, int64_t opitch = 0, int64_t c0 = 0, int64_t c1 = 0,
+                   int maskmode = 0);
 int launch_xgat_st(sg_problem* P, int d, int S_out, int64_t n1, int64_t n2, const StencilOff& so,
                    const uint8_t* xflag, const XgatParams& ep, double* Y, double beta, int m = 0);
 int class_compress(sg_problem* P, const Factor& f, int l, const double* st, double** ctab);
@@ -355,16 +362,16 @@ int launch_fwhole(sg_problem* P, int l1, int l2, int64_t n2, const double* X, do
 // vmoment.cu
 int prepare_vmom(sg_problem* P);
 int launch_vmom(sg_problem* P, int l2, int64_t nrows, int64_t n2, int64_t pitch, const double* X, double* const* outs,
-                const uint8_t* xflag, int64_t n1x);
+                const uint8_t* xflag, int64_t n1x, int64_t c0 = 0, int64_t c1 = 0);
 // xfanin_tma.cu
 int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pitch, const double* Z,
-                      int64_t gstride, double* Y);
+                      int64_t gstride, double* Y, int64_t ypitch = 0, bool stage_tab = true);
 // solver.cu
 int apply_diag(sg_problem* P, const Grid& g, const double* X, double* Y, const double* skip = nullptr);
 int apply_cost(sg_problem* P, const Grid& g, double* bytes, double* flops);
 int count_nnz(sg_problem* P);
 int pass1_vgroups(sg_problem* P, int l1, int l2, const double* X, double* const* outs, int64_t pitch,
-                  double* fbytes = nullptr);
+                  double* fbytes = nullptr, int64_t c0 = 0, int64_t c1 = 0, bool fine_mask = false);
 int apply_cross_prepare(sg_problem* P);
 int apply_cross(sg_problem* P, const std::vector<Term>* terms_override, const double* Tb, int S_out, int S_in,
                 const double* X, double* Y);

@@ -51,7 +51,10 @@ static bool l_has_xfi(const sg_problem* P, int l1) {
 
 // pass 1 of the per-grid operator on grid (l1, l2): Z_o = (Id x Id x B_o) X for every v-group o
 // (vorder; boundary-only groups on x-boundary rows only), written with row pitch `pitch`
-int pass1_vgroups(sg_problem* P, int l1, int l2, const double* X, double* const* outs, int64_t pitch, double* fbytes) {
+int pass1_vgroups(sg_problem* P, int l1, int l2, const double* X, double* const* outs, int64_t pitch, double* fbytes,
+                  int64_t c0, int64_t c1, bool fine_mask) {
+    // columns [c0, c1) of the grid (default: all), written at output columns 0 .. c1 - c0;
+    // fine_mask (diagonal apply): boundary-only groups only on the x-rows of their own faces
     const int S = P->S;
     double fb_dummy = 0.0;
     if (!fbytes) fbytes = &fb_dummy;
@@ -60,6 +63,11 @@ int pass1_vgroups(sg_problem* P, int l1, int l2, const double* X, double* const*
     const int64_t n1 = Lx.n, n2 = Lv.n;
     const int nb = (int)P->vorder.size();
     const bool vbox = P->fv.kind == SG_MESH_BOX && nb <= MAXG;
+    if (c1 <= 0) c1 = n2;
+    const bool whole = c0 == 0 && c1 == n2;
+    const int mm = fine_mask && Lx.bmask && nb - P->ng_int <= 8 ? 1 : 0;
+    const uint8_t* xfl = mm ? Lx.bmask : Lx.bflag;
+    const double cfrac = (double)(c1 - c0) / (double)n2;
     if (vbox) {
         VfanParams vp;
         vp.ng = nb;
@@ -72,8 +80,8 @@ int pass1_vgroups(sg_problem* P, int l1, int l2, const double* X, double* const*
         const bool vmom_here = P->fv.d == 2 || n1 < 64;
         if (vmom_here) {
             // interior groups by shifted moments, boundary-only (face) groups by the stencil kernel
-            rc = launch_vmom(P, l2, (int64_t)S * n1, n2, pitch, X, vp.out, Lx.bflag, n1);
-            if (rc == SG_OK) *fbytes += 8.0 * (double)P->vm_tab_n;   // class tables
+            rc = launch_vmom(P, l2, (int64_t)S * n1, n2, pitch, X, vp.out, Lx.bflag, n1, c0, c1);
+            if (rc == SG_OK && c0 == 0) *fbytes += 8.0 * (double)P->vm_tab_n;   // class tables
             if (rc == SG_OK && nb > P->ng_int && P->vm_nchi == 0) {
                 VfanParams vb;
                 vb.ng = nb - P->ng_int;
@@ -82,17 +90,17 @@ int pass1_vgroups(sg_problem* P, int l1, int l2, const double* X, double* const*
                     vb.vst[o] = vp.vst[P->ng_int + o];
                     vb.out[o] = vp.out[P->ng_int + o];
                 }
-                rc = launch_vfan_st(P, P->fv.d, S, n1, n2, Lv.so, Lx.bflag, vb, X, pitch);
-                *fbytes += 8.0 * vb.ng * P->fv.W * (double)n2;   // per-column stencil coefficients
+                rc = launch_vfan_st(P, P->fv.d, S, n1, n2, Lv.so, xfl, vb, X, pitch, c0, c1, mm);
+                *fbytes += 8.0 * vb.ng * P->fv.W * (double)n2 * cfrac;   // per-column stencil coefficients
             }
         }
         if (rc == SG_ERR_UNSUPPORTED) {
-            rc = launch_vfan_st(P, P->fv.d, S, n1, n2, Lv.so, Lx.bflag, vp, X, pitch);
-            *fbytes += 8.0 * nb * P->fv.W * (double)n2;
+            rc = launch_vfan_st(P, P->fv.d, S, n1, n2, Lv.so, xfl, vp, X, pitch, c0, c1, mm);
+            *fbytes += 8.0 * nb * P->fv.W * (double)n2 * cfrac;
         }
         return rc;
     }
-    if (pitch != n2) return SG_ERR_UNSUPPORTED;
+    if (pitch != n2 || !whole) return SG_ERR_UNSUPPORTED;
     for (int b0 = 0; b0 < nb; b0 += MAX_FANOUT) {
         FanoutList fl;
         fl.no = std::min(MAX_FANOUT, nb - b0);
@@ -145,6 +153,42 @@ static int apply_diag_impl(sg_problem* P, const Grid& g, const double* X, double
     // ---- pass 1: Z_b = (Id x Id x B_b) X for every v-group b (interior groups first)
     // (TMA pass 2 reads the intermediates with an even row pitch)
     const bool tma2 = vbox && xbox && S == 1 && l_has_xfi(P, g.l1);
+    // ---- L2-resident column chunks (north_star subsystem (1): the intermediates
+    // of the two-sided apply are not stored): pass 1 and pass 2 alternate on chunks of v-columns
+    // whose intermediates Z_b (all x-rows x chunk columns x groups) fit in the L2 cache; the same
+    // workspace lines are overwritten chunk after chunk and never leave the L2.
+    if (tma2 && P->l2_chunk_bytes > 0 && P->fx.lev[g.l1].m >= 5) {
+        const int64_t nb1 = Lx.nbnd;
+        const double colbytes = 8.0 * ((double)P->ng_int * g.n1 + (double)(nb - P->ng_int) * nb1);
+        int64_t wc = (int64_t)((double)P->l2_chunk_bytes / colbytes);
+        if (wc < g.n2 && wc >= P->l2_chunk_mincols) {
+            int64_t nch = (g.n2 + wc - 1) / wc;
+            wc = (g.n2 + nch - 1) / nch;
+            wc = (wc + 31) / 32 * 32;   // chunk starts on 256-byte column boundaries of X
+            nch = (g.n2 + wc - 1) / wc;
+            const int64_t pc = wc;      // even row pitch (TMA strides)
+            const int64_t gstr_c = g.n1 * pc;
+            if ((size_t)nb * gstr_c > P->wsZ_n) {
+                set_error("apply_diag: workspace too small");
+                return SG_ERR_STATE;
+            }
+            std::vector<double*> outs(nb);
+            for (int o = 0; o < nb; ++o) outs[o] = P->wsZ + (int64_t)o * gstr_c;
+            for (int64_t ch = 0; ch < nch; ++ch) {
+                const int64_t c0 = ch * wc, c1 = std::min(g.n2, c0 + wc);
+                SG_TRY(pass1_vgroups(P, g.l1, g.l2, X, outs.data(), pc, fbytes, c0, c1, true));
+                int rc2 = launch_xfanin_tma(P, g.l1, g.n1, c1 - c0, pc, P->wsZ, gstr_c, Y + c0, g.n2, ch == 0);
+                if (rc2 != SG_OK) {
+                    if (rc2 == SG_ERR_UNSUPPORTED) set_error("apply_diag: TMA pass 2 rejected a column chunk");
+                    return rc2 == SG_ERR_UNSUPPORTED ? SG_ERR_STATE : rc2;
+                }
+            }
+            int ncls = 1;
+            for (int q = 0; q < P->fx.d; ++q) ncls *= 3;
+            *fbytes += 8.0 * ncls * nb * P->fx.W;
+            return SG_OK;
+        }
+    }
     const int64_t pitch = tma2 ? g.n2 + (g.n2 & 1) : g.n2;
     const int64_t gstr = (int64_t)S * g.n1 * pitch;
     if ((size_t)nb * gstr > P->wsZ_n) {
@@ -154,7 +198,7 @@ static int apply_diag_impl(sg_problem* P, const Grid& g, const double* X, double
     {
         std::vector<double*> outs(nb);
         for (int o = 0; o < nb; ++o) outs[o] = P->wsZ + (int64_t)o * gstr;
-        SG_TRY(pass1_vgroups(P, g.l1, g.l2, X, outs.data(), pitch, fbytes));
+        SG_TRY(pass1_vgroups(P, g.l1, g.l2, X, outs.data(), pitch, fbytes, 0, 0, true));
     }
     // ---- pass 2: Y = sum_b sum_{s,s'} (e_s e_s'^T (x) C_b^{ss'} (x) Id) Z_b
     double beta = 0.0;

@@ -66,7 +66,8 @@ __global__ void __launch_bounds__(256, 2)
     k_vmom(int nthr, int n2, int nrows, int rstride, int m, long long pitch, const double* __restrict__ X,
            const __grid_constant__ VmOut o, const uint8_t* __restrict__ xflag, int n1x,
            const double* __restrict__ tab, const __grid_constant__ VmCoef cf, double lo0, double lo1, double lo2,
-           double h0, double h1, double h2, const double* __restrict__ skip) {
+           double h0, double h1, double h2, const double* __restrict__ skip, int c0, int ncol) {
+    // columns [c0, c0 + ncol) only (L2-resident column chunks); output column a - c0
     if (skip && *skip != 0.0) return;   // grid converged (batched block solver)
     constexpr int W = D == 3 ? 15 : 7;
     constexpr int NC = D == 3 ? 27 : 9;
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(256, 2)
     __syncthreads();
     const int t = blockIdx.x * 256 + threadIdx.x;
     if (t >= nthr) return;
-    const int a = t % n2, q0 = t / n2;
+    const int a = c0 + t % ncol, q0 = t / ncol;
     int z[3] = {a % m, (a / m) % m, D == 3 ? a / (m * m) : 0};
     int cls = 0, mul = 1;
 #pragma unroll
@@ -96,7 +97,7 @@ __global__ void __launch_bounds__(256, 2)
         const int c = a + cf.off[k];
         nb_ok[k] = c >= 0 && c < n2;   // (absent neighbours have zero coefficients)
     }
-    const bool padcol = (a == n2 - 1) && pitch > n2;   // keep the stored rows full 32-byte sectors
+    const bool padcol = (a == c0 + ncol - 1) && pitch > ncol;   // keep the stored rows full 32-byte sectors
     for (int rb = q0 * VR; rb < nrows; rb += rstride * VR) {
         double acc[VM_NP][VR];
 #pragma unroll
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(256, 2)
             double zr[VM_NP];
 #pragma unroll
             for (int n = 0; n < VM_NP; ++n) zr[n] = acc[n][r];
-            const long long idx = (long long)row * pitch + a;
+            const long long idx = (long long)row * pitch + (a - c0);
             vm_combine<D>(zr, y, o, idx);
             const bool xb_row = cf.nchi && xflag[row % n1x];
             if (xb_row) {
@@ -444,8 +445,10 @@ void vmom_coef(const sg_problem* P, int l2, VmCoef* cf, double* lo, double* h) {
 
 // Z_g for the interior v-groups of grid (l1, l2) by moments; SG_ERR_UNSUPPORTED if unavailable
 int launch_vmom(sg_problem* P, int l2, int64_t nrows, int64_t n2, int64_t pitch, const double* X,
-                double* const* outs, const uint8_t* xflag, int64_t n1x) {
+                double* const* outs, const uint8_t* xflag, int64_t n1x, int64_t c0, int64_t c1) {
     if (l2 >= (int)P->vm_ok.size() || !P->vm_ok[l2]) return SG_ERR_UNSUPPORTED;
+    if (c1 <= 0) c1 = n2;
+    const int64_t ncol = c1 - c0;
     const Factor& f = P->fv;
     const Level& L = f.lev[l2];
     const int d = f.d, m = L.m;
@@ -461,8 +464,8 @@ int launch_vmom(sg_problem* P, int l2, int64_t nrows, int64_t n2, int64_t pitch,
     // threads = columns x row blocks (VR rows each), about 16 resident warps per SM
     const long long target = 148LL * 2048;
     const long long rblocks = (nrows + VR - 1) / VR;
-    const int ph = (int)std::max<long long>(1, std::min<long long>(target / n2, rblocks));
-    const long long nthr = n2 * (long long)ph;
+    const int ph = (int)std::max<long long>(1, std::min<long long>(target / ncol, rblocks));
+    const long long nthr = ncol * (long long)ph;
     if (nthr >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
     const unsigned nb = (unsigned)((nthr + 255) / 256);
     const int smb = (d == 3 ? 27 : 9) * ((VM_NP + VM_NC) * W + 1) * (int)sizeof(double);
@@ -470,7 +473,7 @@ int launch_vmom(sg_problem* P, int l2, int64_t nrows, int64_t n2, int64_t pitch,
     do {                                                                                                            \
         cudaFuncSetAttribute(k_vmom<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb);                         \
         k_vmom<DD><<<nb, 256, smb, P->stream>>>((int)nthr, (int)n2, (int)nrows, ph, m, pitch, X, o, xflag, (int)n1x, \
-                                                P->vm_tab[l2], cf, lo[0], lo[1], lo[2], h[0], h[1], h[2], P->skip);          \
+                                                P->vm_tab[l2], cf, lo[0], lo[1], lo[2], h[0], h[1], h[2], P->skip, (int)c0, (int)ncol); \
     } while (0)
     if (d == 3) VMA(3); else VMA(2);
 #undef VMA

@@ -247,11 +247,29 @@ __global__ void __launch_bounds__(256, CPT == 1 ? 2 : 1)
 
 int prepare_xwhole(sg_problem* P);
 
+// per-row mask of the boundary-only (face) groups from the row's boundary class
+struct ClsMask {
+    unsigned char m[27];
+};
+__global__ void k_bmask(int n, int d, int m, ClsMask cm, uint8_t* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int z = i, c = 0, mul = 1;
+    for (int q = 0; q < d; ++q) {
+        const int zq = z % m;
+        z /= m;
+        c += mul * (zq == 0 ? 0 : (zq == m - 1 ? 2 : 1));
+        mul *= 3;
+    }
+    out[i] = cm.m[c];
+}
+
 // host: class tables of the combined x matrices of every v-group (vorder) per x-level
 int prepare_xfanin(sg_problem* P) {
     P->xfi_tab.assign(P->F + 1, nullptr);
     P->xfi_itab.assign(P->F + 1, nullptr);
     P->xfi_cint.assign(P->F + 1, {});
+    P->xfi_cmask.assign(P->F + 1, {});
     if (P->fx.kind != SG_MESH_BOX || P->S != 1 || P->fx.d < 2 ) return SG_OK;
     const int nga = (int)P->vorder.size();
     if (P->ng_int > XFI_MAXG) return SG_OK;
@@ -294,6 +312,48 @@ int prepare_xfanin(sg_problem* P) {
         for (int o = 0; o < P->ng_int; ++o)
             for (int k = 0; k < W; ++k) ci[o * 15 + k] = h[((size_t)icls * nga + o) * W + k];
         P->xfi_cint[l] = ci;
+        // boundary-only groups per boundary class: group j is "present" in class c when a node of that
+        // class has a nonzero coefficient in its row or is the source of one (enumerated on a small
+        // lattice with the same class structure)
+        const int nbo = nga - P->ng_int;
+        const int m = P->fx.lev[l].m;
+        if (nbo >= 0 && nbo <= 8 && m >= 3 && P->fx.lev[l].n < (1LL << 31)) {
+            std::vector<uint8_t> cm(27, 0);
+            const int mq = std::min(m, 5);
+            auto cls_of = [&](const int* z) {
+                int c = 0, mu = 1;
+                for (int q = 0; q < d; ++q) {
+                    c += mu * (z[q] == 0 ? 0 : (z[q] == mq - 1 ? 2 : 1));
+                    mu *= 3;
+                }
+                return c;
+            };
+            int tot = 1;
+            for (int q = 0; q < d; ++q) tot *= mq;
+            for (int i = 0; i < tot; ++i) {
+                int z[3] = {i % mq, (i / mq) % mq, d == 3 ? i / (mq * mq) : 0};
+                const int c = cls_of(z);
+                for (int o = P->ng_int; o < nga; ++o)
+                    for (int k = 0; k < W; ++k) {
+                        if (h[((size_t)c * nga + o) * W + k] == 0.0) continue;
+                        const int dk[3] = {d == 3 ? xfi::d0_3(k) : xfi::d0_2(k), d == 3 ? xfi::d1_3(k) : xfi::d1_2(k),
+                                           d == 3 ? xfi::d2_3(k) : 0};
+                        int zn[3] = {z[0] + dk[0], z[1] + dk[1], z[2] + dk[2]};
+                        bool in = true;
+                        for (int q = 0; q < d; ++q) in &= zn[q] >= 0 && zn[q] < mq;
+                        cm[c] |= (uint8_t)(1u << (o - P->ng_int));
+                        if (in) cm[cls_of(zn)] |= (uint8_t)(1u << (o - P->ng_int));
+                    }
+            }
+            P->xfi_cmask[l] = cm;
+            Level& Lx = P->fx.lev[l];
+            ClsMask cmk;
+            std::memcpy(cmk.m, cm.data(), 27);
+            SG_CUDA(cudaMalloc(&Lx.bmask, Lx.n));
+            k_bmask<<<(unsigned)((Lx.n + 255) / 256), 256, 0, P->stream>>>((int)Lx.n, d, m, cmk, Lx.bmask);
+            P->launches++;
+            SG_CUDA(cudaGetLastError());
+        }
     }
     SG_TRY(prepare_xwhole(P));
     return SG_OK;

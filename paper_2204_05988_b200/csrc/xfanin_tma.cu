@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 
 #include "sg_internal.cuh"
@@ -117,6 +118,10 @@ __constant__ double c_xft[XFT_CTAB];
 struct XftCoef {
     double c[XFT_MAXG][15];
 };
+struct XftMask {
+    int nbo;                   // boundary-only groups (<= 8)
+    unsigned char m[27];       // per boundary class: bit j set when boundary-only group j has a nonzero there
+};
 struct XftTile {
     int wl1, wl2, wc, nw;      // warp blocks per tile (axis 1, axis 2), column groups, consumer warps
     int e1, e2, bc;            // stage box: halo lines (axis 1, axis 2), columns
@@ -127,7 +132,8 @@ struct XftTile {
 template <int D, int NGI, bool CTAB>
 __global__ void __launch_bounds__(32 * 17, 1)
     k_xfanin_tma(const __grid_constant__ CUtensorMap tmap, int nga, int n2, int m, XftTile tl,
-                 const double* __restrict__ tab, const __grid_constant__ XftCoef cint, double* __restrict__ Y, const double* __restrict__ skip) {
+                 const double* __restrict__ tab, const __grid_constant__ XftCoef cint, double* __restrict__ Y, const double* __restrict__ skip,
+                 long long ypitch, const __grid_constant__ XftMask cmask) {
     if (skip && *skip != 0.0) return;   // grid converged (batched block solver)
     using G = xft::Geo<D>;
     constexpr int W = G::W, NT = G::NT, NS = G::NE1 * G::NE2;
@@ -154,6 +160,35 @@ __global__ void __launch_bounds__(32 * 17, 1)
     const bool cta_lines_int = L1 >= 1 && L1 + tl.wl1 * G::B1 - 1 <= m - 2 &&
                                (D == 2 || (L2 >= 1 && L2 + tl.wl2 * G::B2 - 1 <= m - 2));
 
+    // boundary-only (face) groups: a stage (t, g) exists only when some target row of the tile in the
+    // window t-1..t+1 lies in a boundary class where group g is nonzero (producer and consumers agree)
+    unsigned lm[3] = {0u, 0u, 0u};
+    {
+        unsigned s1 = 0, s2 = D == 3 ? 0u : 1u;   // class sets of the tile's target lines per axis
+        for (int i = 0; i < tl.wl1 * G::B1; ++i) {
+            const int z = L1 + i;
+            if (z < m) s1 |= 1u << (z == 0 ? 0 : (z >= m - 1 ? 2 : 1));
+        }
+        if (D == 3)
+            for (int i = 0; i < tl.wl2 * G::B2; ++i) {
+                const int z = L2 + i;
+                if (z < m) s2 |= 1u << (z == 0 ? 0 : (z >= m - 1 ? 2 : 1));
+            }
+        for (int c1 = 0; c1 < 3; ++c1)
+            for (int c2 = 0; c2 < (D == 3 ? 3 : 1); ++c2)
+                if (((s1 >> c1) & 1u) && ((s2 >> c2) & 1u))
+                    for (int c0 = 0; c0 < 3; ++c0) lm[c0] |= cmask.m[c0 + 3 * c1 + 9 * c2];
+    }
+    auto win_mask = [&](const unsigned (&mm)[3], int t) -> unsigned {
+        unsigned r = 0;
+#pragma unroll
+        for (int w = -1; w <= 1; ++w) {
+            const int p = t + w;
+            if (p >= 0 && p < m) r |= mm[p == 0 ? 0 : (p >= m - 1 ? 2 : 1)];
+        }
+        return r;
+    };
+
     if (threadIdx.x == 0) {
         for (int i = 0; i < nst; ++i) {
             xft::mbar_init(&full[i], 1);
@@ -170,9 +205,9 @@ __global__ void __launch_bounds__(32 * 17, 1)
             int q = 0, pb = 0;
             uint32_t pph = 0;
             for (int t = ts; t <= te; ++t) {
-                const bool cint_t = cta_lines_int && t >= 2 && t <= m - 3;
-                const int ng = cint_t ? NGI : nga;
-                for (int g = 0; g < ng; ++g, ++q) {
+                const unsigned cm_t = win_mask(lm, t);
+                for (int g = 0; g < nga; ++g) {
+                    if (g >= NGI && !((cm_t >> (g - NGI)) & 1u)) continue;
                     const int b = pb;
                     if (q >= nst) xft::mbar_wait(&empty[b], pph ^ 1u);
                     if (++pb == nst) {
@@ -186,6 +221,7 @@ __global__ void __launch_bounds__(32 * 17, 1)
                     else
                         xft::tma_load<2>(stages + (size_t)b * stage_elems, &tmap, &full[b], ct * tl.bc, t, L1 - 1, g,
                                          0);
+                    ++q;
                 }
             }
         }
@@ -219,6 +255,12 @@ __global__ void __launch_bounds__(32 * 17, 1)
         tcls12[u] = 3 * c1 + (D == 3 ? 9 * c2 : 0);
         lines_int &= tval[u] && c1 == 1 && (D == 2 || c2 == 1);
     }
+    unsigned wm[3] = {0u, 0u, 0u};   // the warp's own target lines
+#pragma unroll
+    for (int u = 0; u < NT; ++u)
+        if (tval[u])
+#pragma unroll
+            for (int c0 = 0; c0 < 3; ++c0) wm[c0] |= cmask.m[c0 + tcls12[u]];
     double acc[NT][3];
 #pragma unroll
     for (int u = 0; u < NT; ++u) acc[u][0] = acc[u][1] = acc[u][2] = 0.0;
@@ -226,7 +268,7 @@ __global__ void __launch_bounds__(32 * 17, 1)
     int q = 0, cbuf = 0;
     uint32_t cph = 0;
     for (int t = ts; t <= te; ++t) {
-        const bool cint_t = cta_lines_int && t >= 2 && t <= m - 3;
+        const unsigned cm_t = win_mask(lm, t), wm_t = win_mask(wm, t);
         const bool wint = lines_int && t >= 2 && t <= m - 3;
         int cb[NT][3], cbi[NT][3];
 #pragma unroll
@@ -281,15 +323,17 @@ __global__ void __launch_bounds__(32 * 17, 1)
             __syncwarp();
             if (lane == 0) xft::mbar_arrive(&empty[b]);
         }
-        if (!cint_t) {
-            for (int g = NGI; g < nga; ++g, ++q) {
+        if (cm_t) {
+            for (int g = NGI; g < nga; ++g) {
+                if (!((cm_t >> (g - NGI)) & 1u)) continue;
+                ++q;
                 const int b = cbuf;
                 xft::mbar_wait(&full[b], cph);
                 if (++cbuf == nst) {
                     cbuf = 0;
                     cph ^= 1u;
                 }
-                if (!wint) {
+                if ((wm_t >> (g - NGI)) & 1u) {
                     const double* st = stages + (size_t)b * stage_elems;
                     const double* tg = tab + g * W;
                     double src[NS];
@@ -315,7 +359,7 @@ __global__ void __launch_bounds__(32 * 17, 1)
         if (t - 1 >= t0 && cval) {
 #pragma unroll
             for (int u = 0; u < NT; ++u)
-                if (tval[u]) Y[((long long)(t - 1) + (long long)m * tline[u]) * n2 + col] = acc[u][0];
+                if (tval[u]) Y[((long long)(t - 1) + (long long)m * tline[u]) * ypitch + col] = acc[u][0];
         }
 #pragma unroll
         for (int u = 0; u < NT; ++u) {
@@ -327,7 +371,7 @@ __global__ void __launch_bounds__(32 * 17, 1)
     if (t1 == m && cval) {
 #pragma unroll
         for (int u = 0; u < NT; ++u)
-            if (tval[u]) Y[((long long)(m - 1) + (long long)m * tline[u]) * n2 + col] = acc[u][0];
+            if (tval[u]) Y[((long long)(m - 1) + (long long)m * tline[u]) * ypitch + col] = acc[u][0];
     }
 }
 
@@ -378,7 +422,14 @@ static XftTile choose_tile(int d, int m, int64_t n2, int force_wc, int box_kb) {
 }
 
 int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pitch, const double* Z,
-                      int64_t gstride, double* Y) {
+                      int64_t gstride, double* Y, int64_t ypitch, bool stage_tab) {
+    if (l1 >= (int)P->xfi_cmask.size() || P->xfi_cmask[l1].size() != 27) return SG_ERR_UNSUPPORTED;
+    XftMask cmk;
+    cmk.nbo = (int)P->vorder.size() - P->ng_int;
+    if (cmk.nbo > 8) return SG_ERR_UNSUPPORTED;
+    std::memcpy(cmk.m, P->xfi_cmask[l1].data(), 27);
+    // n2 columns of Z (row pitch `pitch`) -> n2 columns of Y (row pitch ypitch: a column chunk of a wider grid)
+    if (ypitch <= 0) ypitch = n2;
     if (l1 >= (int)P->xfi_tab.size() || !P->xfi_tab[l1]) return SG_ERR_UNSUPPORTED;
     const int d = P->fx.d, m = P->fx.lev[l1].m;
     const int nga = (int)P->vorder.size(), ngi = P->ng_int;
@@ -388,16 +439,22 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
     if (!enc) return SG_ERR_UNSUPPORTED;
     // wide boxes (4 column groups = 1 KB rows) measured fastest on the m >= 9 lattices
     // (grid (5,3): 1.67 -> 1.25 ms) and slowest on m = 5 (3.3 -> 4.7 ms)
-    const int wc_auto = (m >= 9 && n2 >= 128) ? 4 : 0;
+    int wc_auto = (m >= 9 && n2 >= 128) ? 4 : 0;
+    static const int e_wc = getenv("SG_XFT_WC") ? atoi(getenv("SG_XFT_WC")) : -1;
+    static const int e_kb = getenv("SG_XFT_KB") ? atoi(getenv("SG_XFT_KB")) : -1;
+    static const int e_nst = getenv("SG_XFT_NST") ? atoi(getenv("SG_XFT_NST")) : -1;
+    static const int e_cta = getenv("SG_XFT_CTA") ? atoi(getenv("SG_XFT_CTA")) : 3;
+    if (e_wc >= 0 && m >= 9 && n2 >= 32 * e_wc) wc_auto = e_wc;
     // ... and small CTAs (one 2x2 line block x 4 column groups, 16 KB stages) beat larger tiles
     // on those lattices: more independent TMA producers per SM (grid (3,5): 2.02 -> 1.82 ms)
-    const int box_kb = wc_auto ? (d == 3 ? 16 : 8) : 24;
+    int box_kb = wc_auto ? (d == 3 ? 16 : 8) : 24;
+    if (e_kb > 0 && m >= 9) box_kb = e_kb;
     XftTile tl = choose_tile(d, m, n2, wc_auto, box_kb);
     if (tl.nw == 0) tl = choose_tile(d, m, n2, 0, 24);
     // split the sweep until there are >= 2 CTAs per SM
     const int64_t base = (int64_t)tl.ntl1 * tl.ntl2 * tl.nct;
     int seglen = m;
-    while (seglen > 8 && base * ((m + seglen - 1) / seglen) < 148 * 3) seglen = (seglen + 1) / 2;
+    while (seglen > 8 && base * ((m + seglen - 1) / seglen) < 148 * e_cta) seglen = (seglen + 1) / 2;
     tl.seglen = seglen;
     tl.nseg = (m + seglen - 1) / seglen;
     const int64_t nblk = base * tl.nseg;
@@ -436,12 +493,17 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
     // 4 stages measured best (deeper rings shrink L1 and were slower: (2,6) 3.3 -> 5.1 ms at 8 stages)
     // (3 stages on the wide-box 3D tiles: 1.2 % faster than 4)
     tl.nst = wc_auto && d == 3 ? 3 : 4;
+    if (e_nst > 0) tl.nst = e_nst;
+    if (P->verbose)
+        fprintf(stderr, "xft l1=%d m=%d n2=%lld tile w1=%d w2=%d wc=%d nw=%d box=%dx%dx%d nst=%d seglen=%d nblk=%lld\n", l1, m,
+                (long long)n2, tl.wl1, tl.wl2, tl.wc, tl.nw, tl.e1, tl.e2, tl.bc, tl.nst, tl.seglen, (long long)nblk);
     const size_t smem = (size_t)tl.nst * stage_b + 2 * tl.nst * sizeof(uint64_t);
     {
         int ncls = 1;
         for (int q = 0; q < d; ++q) ncls *= 3;
         const size_t nt = (size_t)ncls * ngi * P->fx.W;
         if (nt > (size_t)XFT_CTAB || !P->xfi_itab[l1]) return SG_ERR_UNSUPPORTED;
+        if (stage_tab)   // (later column chunks of the same apply reuse the staged table)
         SG_CUDA(cudaMemcpyToSymbolAsync(c_xft, P->xfi_itab[l1], sizeof(double) * nt, 0, cudaMemcpyDeviceToDevice,
                                         P->stream));
     }
@@ -450,7 +512,7 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
 #define XFT(DD, NG, CT)                                                                                          \
     do {                                                                                                         \
         cudaFuncSetAttribute(k_xfanin_tma<DD, NG, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-        k_xfanin_tma<DD, NG, CT><<<(unsigned)nblk, threads, smem, P->stream>>>(tm, nga, (int)n2, m, tl, tab, ci, Y, P->skip); \
+        k_xfanin_tma<DD, NG, CT><<<(unsigned)nblk, threads, smem, P->stream>>>(tm, nga, (int)n2, m, tl, tab, ci, Y, P->skip, (long long)ypitch, cmk); \
     } while (0)
     const bool ctab = m >= 9;
     if (d == 3) {
