@@ -147,6 +147,82 @@ __global__ void __launch_bounds__(256) k_gather_s2(int64_t n1_in, int64_t n2_in,
     }
 }
 
+// ... the same with CPT columns per thread (columns lane, lane + 32, ... of a 32*CPT-wide tile): a warp
+// works on ONE row r, so every coefficient load (warp-uniform broadcast) feeds CPT multiply-adds
+// and the pattern row is read once per warp tile.
+template <int W, int CPT>
+__global__ void __launch_bounds__(256) k_gather_s2c(int64_t n1_in, int64_t n2_in, int64_t n1_out,
+                                                    const int32_t* __restrict__ cols,
+                                                    const __grid_constant__ EntryList el, double* __restrict__ out,
+                                                    double beta, int ncoltiles, const double* __restrict__ skip) {
+    if (skip && *skip != 0.0) return;   // grid converged (batched block solver)
+    const int lane = threadIdx.x & 31;
+    // block = 8 consecutive rows x one column tile: neighbouring rows share their sources through L1
+    const long long nrb = (n1_out + 7) / 8, nblk = nrb * ncoltiles;
+    const size_t per_in = (size_t)n1_in * n2_in, per_out = (size_t)n1_out * n2_in;
+    for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const int ct = (int)(blk % ncoltiles);
+        const long long rr = (blk / ncoltiles) * 8 + (threadIdx.x >> 5);
+        if (rr >= n1_out) continue;
+        const int r = (int)rr;
+        int32_t cl[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) cl[k] = __ldg(cols + (size_t)k * n1_out + r);
+        int c[CPT];
+        bool cv[CPT];
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) {
+            c[j] = ct * 32 * CPT + j * 32 + lane;
+            cv[j] = c[j] < n2_in;
+            if (!cv[j]) c[j] = 0;
+        }
+        double acc0[CPT], acc1[CPT], xv[W][CPT];
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) acc0[j] = acc1[j] = 0.0;
+        const double* prev = nullptr;
+        int prev_s = -1;
+        for (int e = 0; e < el.ne; ++e) {
+            const Entry& E = el.e[e];
+            if (E.in != prev || E.s_in != prev_s) {
+                prev = E.in;
+                prev_s = E.s_in;
+                const double* base = E.in + (size_t)E.s_in * per_in;
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                    const double* row = base + (size_t)(cl[k] >= 0 ? cl[k] : 0) * n2_in;
+#pragma unroll
+                    for (int j = 0; j < CPT; ++j) xv[k][j] = cl[k] >= 0 ? __ldg(row + c[j]) : 0.0;
+                }
+            }
+            const double* v = E.vals + r;
+            double a2[CPT];
+#pragma unroll
+            for (int j = 0; j < CPT; ++j) a2[j] = 0.0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                const double cf = __ldg(v + (size_t)k * n1_out);   // (zero where the neighbour is absent)
+#pragma unroll
+                for (int j = 0; j < CPT; ++j) a2[j] = fma(cf, xv[k][j], a2[j]);
+            }
+            if (E.s_out == 0) {
+#pragma unroll
+                for (int j = 0; j < CPT; ++j) acc0[j] = fma(E.scale, a2[j], acc0[j]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < CPT; ++j) acc1[j] = fma(E.scale, a2[j], acc1[j]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) {
+            if (!cv[j]) continue;
+            double* y0 = out + (size_t)r * n2_in + c[j];
+            double* y1 = y0 + per_out;
+            *y0 = beta == 0.0 ? acc0[j] : fma(beta, *y0, acc0[j]);
+            *y1 = beta == 0.0 ? acc1[j] : fma(beta, *y1, acc1[j]);
+        }
+    }
+}
+
 static int grid_for(int64_t total) {
     int64_t b = (total + 255) / 256;
     if (b > 148 * 64) b = 148 * 64;
@@ -218,6 +294,23 @@ int launch_gather(sg_problem* P, int dir, int W, int S_out, int64_t n1_in, int64
             return a.in != b.in ? a.in < b.in : a.s_in < b.s_in;
         });
         es.sbeg[0] = es.sbeg[1] = es.sbeg[2] = 0;
+        if (W == 7 && n2_in >= 128) {   // (narrower grids: the flattened kernel below measured faster)
+            // several columns per thread: one coefficient load per CPT multiply-adds
+            // (tile width chosen for the least padding)
+            const int64_t pad4 = (n2_in + 127) / 128 * 128, pad2 = (n2_in + 63) / 64 * 64;
+            const int cpt = pad4 <= pad2 ? 4 : 2;
+            const int64_t nct = (n2_in + 32 * cpt - 1) / (32 * cpt);
+            const int64_t nblk = std::min<int64_t>((nrows_out + 7) / 8 * nct, 148 * 64);
+            if (cpt == 4)
+                k_gather_s2c<7, 4><<<(unsigned)nblk, 256, 0, P->stream>>>(n1_in, n2_in, nrows_out, cols, es, out, beta,
+                                                                          (int)nct, P->skip);
+            else
+                k_gather_s2c<7, 2><<<(unsigned)nblk, 256, 0, P->stream>>>(n1_in, n2_in, nrows_out, cols, es, out, beta,
+                                                                          (int)nct, P->skip);
+            P->launches++;
+            SG_CUDA(cudaGetLastError());
+            return SG_OK;
+        }
         const int g = grid_for(nrows_out * n2_in);
 #define GS2(WW) k_gather_s2<WW><<<g, 256, 0, P->stream>>>(n1_in, n2_in, nrows_out, cols, es, out, beta, P->skip)
         if (W == 3) GS2(3); else if (W == 7) GS2(7); else if (W == 15) GS2(15); else if (W == 2) GS2(2);
