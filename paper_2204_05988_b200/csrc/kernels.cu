@@ -458,7 +458,7 @@ int launch_ell_to_stencil(sg_problem* P, int64_t n, int W, const int32_t* cols, 
 // index >= ng_int are only needed on x-boundary rows (face terms).
 constexpr int VF_TC = 32;   // columns per block
 constexpr int VF_RL = 8;    // row lanes per block
-template <int D, int R, int MINB = 2>
+template <int D, int R, int MINB = 2, int NGI = 0>
 __global__ void __launch_bounds__(VF_TC * VF_RL, MINB) k_vfan_st(int64_t nrows, int64_t n1, int64_t n2, StencilOff so,
                                                               const uint8_t* __restrict__ xflag, VfanParams vp,
                                                               const double* __restrict__ X, int64_t rows_per_block,
@@ -512,9 +512,7 @@ __global__ void __launch_bounds__(VF_TC * VF_RL, MINB) k_vfan_st(int64_t nrows, 
             if (row < re) rm |= xflag[one_s ? row : row % n1i];
         }
         const unsigned long long bneed = maskmode ? (unsigned long long)rm : (rm ? ~0ULL : 0ULL);
-        const int ngu = bneed ? vp.ng : vp.ng_int;
-        for (int g = 0; g < ngu; ++g) {
-            if (g >= vp.ng_int && !((bneed >> (g - vp.ng_int)) & 1ULL)) continue;
+        auto group = [&](int g) {
             double acc[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) acc[r] = 0.0;
@@ -528,7 +526,18 @@ __global__ void __launch_bounds__(VF_TC * VF_RL, MINB) k_vfan_st(int64_t nrows, 
 #pragma unroll
             for (int r = 0; r < R; ++r)
                 if (r0 + r < re && aval) o[r * opitch] = acc[r];
+        };
+        if (NGI > 0) {
+            // interior groups: compile-time count (unrolled: immediate shared-memory offsets and
+            // output pointers from the parameter bank)
+#pragma unroll
+            for (int g = 0; g < NGI; ++g) group(g);
+        } else {
+            for (int g = 0; g < vp.ng_int; ++g) group(g);
         }
+        if (bneed)
+            for (int g = vp.ng_int; g < vp.ng; ++g)
+                if ((bneed >> (g - vp.ng_int)) & 1ULL) group(g);
     }
 }
 
@@ -964,8 +973,15 @@ int launch_vfan_st(sg_problem* P, int d, int S, int64_t n1, int64_t n2, const St
         k_vfan_st<2, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch, P->skip, c0, c1, maskmode);
     } else {
         // R = 2 rows per thread (R = 3/4 measured 4-11 % slower in round 1: register-starved)
-        cudaFuncSetAttribute(k_vfan_st<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_vfan_st<3, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch, P->skip, c0, c1, maskmode);
+        if (vp.ng_int == 10) {
+            cudaFuncSetAttribute(k_vfan_st<3, 2, 2, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_vfan_st<3, 2, 2, 10><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch, P->skip, c0,
+                                                                     c1, maskmode);
+        } else {
+            cudaFuncSetAttribute(k_vfan_st<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_vfan_st<3, 2><<<grid, block, smem, P->stream>>>(nrows, n1, n2, so, xflag, vp, X, rpb, opitch, P->skip, c0, c1,
+                                                              maskmode);
+        }
     }
     P->launches++;
     SG_CUDA(cudaGetLastError());

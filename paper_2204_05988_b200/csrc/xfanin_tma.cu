@@ -127,6 +127,7 @@ struct XftTile {
     int e1, e2, bc;            // stage box: halo lines (axis 1, axis 2), columns
     int ntl1, ntl2, nct, nseg, seglen;
     int nst;                   // pipeline depth
+    int np;                    // producer lanes (each loads 1/np of the stage box along the slowest line axis)
 };
 
 template <int D, int NGI, bool CTAB>
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(32 * 17, 1)
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < nst; ++i) {
-            xft::mbar_init(&full[i], 1);
+            xft::mbar_init(&full[i], tl.np);
             xft::mbar_init(&empty[i], tl.nw);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -199,9 +200,12 @@ __global__ void __launch_bounds__(32 * 17, 1)
     __syncthreads();
 
     if (warp == tl.nw) {
-        // ---------------- producer: one elected lane issues the TMA loads
-        if (lane == 0) {
-            const uint32_t bytes = (uint32_t)stage_elems * 8u;
+        // ---------------- producer: np elected lanes, each issues the TMA load of its slice of
+        // the stage box (loads issued by one thread were measured to overlap poorly)
+        if (lane < tl.np) {
+            const int esplit = (D == 3 ? tl.e2 : tl.e1) / tl.np;          // lines of the split axis per slice
+            const int slice_elems = stage_elems / tl.np;
+            const uint32_t bytes = (uint32_t)slice_elems * 8u;
             int q = 0, pb = 0;
             uint32_t pph = 0;
             for (int t = ts; t <= te; ++t) {
@@ -215,12 +219,11 @@ __global__ void __launch_bounds__(32 * 17, 1)
                         pph ^= 1u;
                     }
                     xft::mbar_expect_tx(&full[b], bytes);
+                    double* dst = stages + (size_t)b * stage_elems + (size_t)lane * slice_elems;
                     if (D == 3)
-                        xft::tma_load<3>(stages + (size_t)b * stage_elems, &tmap, &full[b], ct * tl.bc, t, L1 - 1,
-                                         L2 - 1, g);
+                        xft::tma_load<3>(dst, &tmap, &full[b], ct * tl.bc, t, L1 - 1, L2 - 1 + lane * esplit, g);
                     else
-                        xft::tma_load<2>(stages + (size_t)b * stage_elems, &tmap, &full[b], ct * tl.bc, t, L1 - 1, g,
-                                         0);
+                        xft::tma_load<2>(dst, &tmap, &full[b], ct * tl.bc, t, L1 - 1 + lane * esplit, g, 0);
                     ++q;
                 }
             }
@@ -396,7 +399,8 @@ static XftTile choose_tile(int d, int m, int64_t n2, int force_wc, int box_kb) {
     double best_cost = 1e30;
     const int B1 = d == 3 ? 2 : 4;
     const int lines1 = m, lines2 = d == 3 ? m : 1;
-    for (int wc = 1; wc <= 4; wc *= 2) {
+    for (int wc = 1; wc <= 8; wc *= 2) {
+        if (wc == 8 && force_wc != 8) continue;
         if (wc > 1 && n2 < 32LL * wc) continue;
         if (force_wc > 0 && wc != force_wc) continue;
         for (int w1 = 1; w1 <= 16; ++w1)
@@ -443,10 +447,11 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
     static const int e_wc = getenv("SG_XFT_WC") ? atoi(getenv("SG_XFT_WC")) : -1;
     static const int e_kb = getenv("SG_XFT_KB") ? atoi(getenv("SG_XFT_KB")) : -1;
     static const int e_nst = getenv("SG_XFT_NST") ? atoi(getenv("SG_XFT_NST")) : -1;
-    static const int e_cta = getenv("SG_XFT_CTA") ? atoi(getenv("SG_XFT_CTA")) : 3;
+    static const int e_np = getenv("SG_XFT_NP") ? atoi(getenv("SG_XFT_NP")) : 1;
     if (e_wc >= 0 && m >= 9 && n2 >= 32 * e_wc) wc_auto = e_wc;
     // ... and small CTAs (one 2x2 line block x 4 column groups, 16 KB stages) beat larger tiles
     // on those lattices: more independent TMA producers per SM (grid (3,5): 2.02 -> 1.82 ms)
+    // (round-2 sweeps profiles/r2g, r2m: 4x6 / 4x8 / 6x6-line boxes with 2-6 stages are equal or slower)
     int box_kb = wc_auto ? (d == 3 ? 16 : 8) : 24;
     if (e_kb > 0 && m >= 9) box_kb = e_kb;
     XftTile tl = choose_tile(d, m, n2, wc_auto, box_kb);
@@ -454,8 +459,13 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
     // split the sweep until there are >= 2 CTAs per SM
     const int64_t base = (int64_t)tl.ntl1 * tl.ntl2 * tl.nct;
     int seglen = m;
-    while (seglen > 8 && base * ((m + seglen - 1) / seglen) < 148 * e_cta) seglen = (seglen + 1) / 2;
+    while (seglen > 8 && base * ((m + seglen - 1) / seglen) < 148 * 3) seglen = (seglen + 1) / 2;
     tl.seglen = seglen;
+    tl.np = 1;
+    {
+        const int es = d == 3 ? tl.e2 : tl.e1;
+        if (e_np > 1 && es % e_np == 0 && m >= 9) tl.np = e_np;
+    }
     tl.nseg = (m + seglen - 1) / seglen;
     const int64_t nblk = base * tl.nseg;
     if (nblk >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
@@ -471,14 +481,14 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
         strides[1] = (cuuint64_t)pitch * 8 * m;
         strides[2] = (cuuint64_t)pitch * 8 * m * m;
         strides[3] = (cuuint64_t)gstride * 8;
-        box[0] = tl.bc; box[1] = 1; box[2] = tl.e1; box[3] = tl.e2; box[4] = 1;
+        box[0] = tl.bc; box[1] = 1; box[2] = tl.e1; box[3] = tl.e2 / tl.np; box[4] = 1;
     } else {
         rank = 4;
         dims[0] = (cuuint64_t)n2; dims[1] = m; dims[2] = m; dims[3] = nga;
         strides[0] = (cuuint64_t)pitch * 8;
         strides[1] = (cuuint64_t)pitch * 8 * m;
         strides[2] = (cuuint64_t)gstride * 8;
-        box[0] = tl.bc; box[1] = 1; box[2] = tl.e1; box[3] = 1;
+        box[0] = tl.bc; box[1] = 1; box[2] = tl.e1 / tl.np; box[3] = 1;
     }
     CUresult cr = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double*>(Z), dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -495,8 +505,8 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
     tl.nst = wc_auto && d == 3 ? 3 : 4;
     if (e_nst > 0) tl.nst = e_nst;
     if (P->verbose)
-        fprintf(stderr, "xft l1=%d m=%d n2=%lld tile w1=%d w2=%d wc=%d nw=%d box=%dx%dx%d nst=%d seglen=%d nblk=%lld\n", l1, m,
-                (long long)n2, tl.wl1, tl.wl2, tl.wc, tl.nw, tl.e1, tl.e2, tl.bc, tl.nst, tl.seglen, (long long)nblk);
+        fprintf(stderr, "xft l1=%d m=%d n2=%lld tile w1=%d w2=%d wc=%d nw=%d box=%dx%dx%d nst=%d seglen=%d np=%d nblk=%lld\n", l1, m,
+                (long long)n2, tl.wl1, tl.wl2, tl.wc, tl.nw, tl.e1, tl.e2, tl.bc, tl.nst, tl.seglen, tl.np, (long long)nblk);
     const size_t smem = (size_t)tl.nst * stage_b + 2 * tl.nst * sizeof(uint64_t);
     {
         int ncls = 1;

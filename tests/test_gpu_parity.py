@@ -302,8 +302,9 @@ def test_apply_strip_operator_kernel_paths(name, env, monkeypatch):
     of the fused whole-x apply (moment pass 1 + whole-x pass 2)."""
     from oracle.sgrid import SGProblem
     from paper_2204_05988_b200 import Problem
-    key, _, val = env.partition("=")
-    monkeypatch.setenv(key, val or "1")
+    for kv in env.split(";"):
+        key, _, val = kv.partition("=")
+        monkeypatch.setenv(key, val or "1")
     cfg = get_config(name, L=SMALL[name])
     g, o = Problem(cfg), SGProblem(cfg)
     rng = np.random.default_rng(5)
@@ -349,15 +350,21 @@ def test_apply_strip_operator_full_size():
     assert relmax(Yt.cpu().numpy().reshape(X.shape), ref) <= 1e-12
 
 
+@pytest.mark.parametrize("chunk_mb", [None, "1"])
 @pytest.mark.parametrize("name,L", [("c2_4d_stream", 8), ("c4_6d_stream", 5)])
-def test_apply_strip_operator_fused_sizes(name, L):
+def test_apply_strip_operator_fused_sizes(name, L, chunk_mb, monkeypatch):
     """Every active and coarse grid at a level where the fused whole-x kernel engages on many
     column blocks with a ragged tail (configs[2] L = 8: level-1/2 x-lattices (1,7), (2,6), ...;
     configs[4] L = 5: (1,4), (1,3)) next to the two-pass kernels of the other grids, element by
-    element against the oracle (factors assembled on each grid's own levels)."""
+    element against the oracle (factors assembled on each grid's own levels).  chunk_mb: the
+    opt-in L2-resident column-chunk pipeline with 1 MB chunks, i.e. 5-8
+    chunks with a ragged last one on grids such as (4,4) / (2,3)."""
     from oracle.problem import delta_hmin, strip_terms
     from oracle.sgrid import SGProblem
     from paper_2204_05988_b200 import Problem
+    if chunk_mb:
+        monkeypatch.setenv("SG_L2_MB", chunk_mb)
+        monkeypatch.setenv("SG_L2_MINCOLS", "32")
     cfg = get_config(name, L=L)
     g, o = Problem(cfg), SGProblem(cfg, galerkin="direct")
     rng = np.random.default_rng(31)
