@@ -144,6 +144,14 @@ __global__ void __launch_bounds__(32 * 17, 1)
     const int nst = tl.nst;
     uint64_t* full = reinterpret_cast<uint64_t*>(smraw + (size_t)nst * stage_elems * 8);
     uint64_t* empty = full + nst;
+    // tiny all-boundary lattices (!CTAB): the class table [3^D][groups][W] lives in shared memory
+    // (every coefficient is a warp-uniform broadcast load; the global table cost a 64-bit address
+    // computation and an L1 lookup per multiply-add)
+    double* stab = reinterpret_cast<double*>(smraw + (size_t)nst * stage_elems * 8 + 2 * (size_t)nst * sizeof(uint64_t));
+    if (!CTAB) {
+        const int ntab = (D == 3 ? 27 : 9) * nga * G::W;
+        for (int i = threadIdx.x; i < ntab; i += blockDim.x) stab[i] = __ldg(tab + i);
+    }
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // CTA -> (line tile, segment, column tile)
@@ -310,7 +318,7 @@ __global__ void __launch_bounds__(32 * 17, 1)
             } else {
                 // near the boundary: constant-cache table when boundary steps are a minority
                 // (m >= 9), global class table (L1 broadcast) on the tiny all-boundary lattices
-                const double* tg = CTAB ? c_xft + g * W : tab + g * W;
+                const double* tg = CTAB ? c_xft + g * W : stab + g * W;
 #pragma unroll
                 for (int s = 0; s < NS; ++s)
 #pragma unroll
@@ -319,7 +327,7 @@ __global__ void __launch_bounds__(32 * 17, 1)
                         for (int k = 0; k < W; ++k)
                             if (xft::pair_ok<D>(s, u, k)) {
                                 const int slot = 1 - G::d0(k);
-                                const double cf = CTAB ? tg[cbi[u][slot] + k] : __ldg(tg + cb[u][slot] + k);
+                                const double cf = CTAB ? tg[cbi[u][slot] + k] : tg[cb[u][slot] + k];
                                 acc[u][slot] = fma(cf, src[s], acc[u][slot]);
                             }
             }
@@ -338,7 +346,7 @@ __global__ void __launch_bounds__(32 * 17, 1)
                 }
                 if ((wm_t >> (g - NGI)) & 1u) {
                     const double* st = stages + (size_t)b * stage_elems;
-                    const double* tg = tab + g * W;
+                    const double* tg = CTAB ? tab + g * W : stab + g * W;
                     double src[NS];
 #pragma unroll
                     for (int s = 0; s < NS; ++s)
@@ -351,7 +359,8 @@ __global__ void __launch_bounds__(32 * 17, 1)
                             for (int k = 0; k < W; ++k)
                                 if (xft::pair_ok<D>(s, u, k)) {
                                     const int slot = 1 - G::d0(k);
-                                    acc[u][slot] = fma(__ldg(tg + cb[u][slot] + k), src[s], acc[u][slot]);
+                                    acc[u][slot] = fma(CTAB ? __ldg(tg + cb[u][slot] + k) : tg[cb[u][slot] + k], src[s],
+                                                       acc[u][slot]);
                                 }
                 }
                 __syncwarp();
@@ -443,17 +452,13 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
     if (!enc) return SG_ERR_UNSUPPORTED;
     // wide boxes (4 column groups = 1 KB rows) measured fastest on the m >= 9 lattices
     // (grid (5,3): 1.67 -> 1.25 ms) and slowest on m = 5 (3.3 -> 4.7 ms)
-    int wc_auto = (m >= 9 && n2 >= 128) ? 4 : 0;
-    static const int e_wc = getenv("SG_XFT_WC") ? atoi(getenv("SG_XFT_WC")) : -1;
-    static const int e_kb = getenv("SG_XFT_KB") ? atoi(getenv("SG_XFT_KB")) : -1;
-    static const int e_nst = getenv("SG_XFT_NST") ? atoi(getenv("SG_XFT_NST")) : -1;
-    static const int e_np = getenv("SG_XFT_NP") ? atoi(getenv("SG_XFT_NP")) : 1;
-    if (e_wc >= 0 && m >= 9 && n2 >= 32 * e_wc) wc_auto = e_wc;
+    // (3D: 8 column groups = 2 KB rows, the TMA box limit of 256 elements, are 4-15 % faster still:
+    // (3,5) 1.59 -> 1.34 ms, (4,4) 1.10 -> 1.00 ms, profiles/r2o, r2p; no gain on the 2D lattices)
+    const int wc_auto = (m >= 9 && n2 >= 128) ? ((d == 3 && n2 >= 256) ? 8 : 4) : 0;
     // ... and small CTAs (one 2x2 line block x 4 column groups, 16 KB stages) beat larger tiles
     // on those lattices: more independent TMA producers per SM (grid (3,5): 2.02 -> 1.82 ms)
     // (round-2 sweeps profiles/r2g, r2m: 4x6 / 4x8 / 6x6-line boxes with 2-6 stages are equal or slower)
-    int box_kb = wc_auto ? (d == 3 ? 16 : 8) : 24;
-    if (e_kb > 0 && m >= 9) box_kb = e_kb;
+    const int box_kb = wc_auto ? (d == 3 ? (wc_auto == 8 ? 32 : 16) : 8) : 24;
     XftTile tl = choose_tile(d, m, n2, wc_auto, box_kb);
     if (tl.nw == 0) tl = choose_tile(d, m, n2, 0, 24);
     // split the sweep until there are >= 2 CTAs per SM
@@ -461,11 +466,7 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
     int seglen = m;
     while (seglen > 8 && base * ((m + seglen - 1) / seglen) < 148 * 3) seglen = (seglen + 1) / 2;
     tl.seglen = seglen;
-    tl.np = 1;
-    {
-        const int es = d == 3 ? tl.e2 : tl.e1;
-        if (e_np > 1 && es % e_np == 0 && m >= 9) tl.np = e_np;
-    }
+    tl.np = 1;   // (2-6 producer lanes per stage measured no different, profiles/r2o)
     tl.nseg = (m + seglen - 1) / seglen;
     const int64_t nblk = base * tl.nseg;
     if (nblk >= (1LL << 31)) return SG_ERR_UNSUPPORTED;
@@ -503,11 +504,16 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
     // 4 stages measured best (deeper rings shrink L1 and were slower: (2,6) 3.3 -> 5.1 ms at 8 stages)
     // (3 stages on the wide-box 3D tiles: 1.2 % faster than 4)
     tl.nst = wc_auto && d == 3 ? 3 : 4;
-    if (e_nst > 0) tl.nst = e_nst;
     if (P->verbose)
         fprintf(stderr, "xft l1=%d m=%d n2=%lld tile w1=%d w2=%d wc=%d nw=%d box=%dx%dx%d nst=%d seglen=%d np=%d nblk=%lld\n", l1, m,
                 (long long)n2, tl.wl1, tl.wl2, tl.wc, tl.nw, tl.e1, tl.e2, tl.bc, tl.nst, tl.seglen, tl.np, (long long)nblk);
-    const size_t smem = (size_t)tl.nst * stage_b + 2 * tl.nst * sizeof(uint64_t);
+    // class table of the boundary path: constant bank where boundary steps are a minority, shared
+    // memory on the small lattices (3D m = 5: pass 2 of grid (2,6) 2.80 -> 1.93 ms; 2D m <= 17:
+    // 0.38 -> 0.33 ms on (3,9); the 52 KB 3D table costs too much occupancy from m = 9 on; profiles/r2r)
+    const bool ctab = d == 3 ? m >= 9 : m >= 33;
+    if (!ctab && d == 3) tl.nst = 3;   // room for two CTAs per SM next to the 52 KB shared-memory class table
+    size_t smem = (size_t)tl.nst * stage_b + 2 * tl.nst * sizeof(uint64_t);
+    if (!ctab) smem += sizeof(double) * (d == 3 ? 27 : 9) * nga * P->fx.W;
     {
         int ncls = 1;
         for (int q = 0; q < d; ++q) ncls *= 3;
@@ -524,7 +530,6 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
         cudaFuncSetAttribute(k_xfanin_tma<DD, NG, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         k_xfanin_tma<DD, NG, CT><<<(unsigned)nblk, threads, smem, P->stream>>>(tm, nga, (int)n2, m, tl, tab, ci, Y, P->skip, (long long)ypitch, cmk); \
     } while (0)
-    const bool ctab = m >= 9;
     if (d == 3) {
         if (ctab) XFT(3, 10, true); else XFT(3, 10, false);
     } else {
