@@ -1082,6 +1082,7 @@ __global__ void __launch_bounds__(256) k_jobs_rbox(JobList jl) {
         const unsigned s = t >= per_s ? 1u : 0u;
         const unsigned rc = t - s * per_s;
         const unsigned r = rc / n2_out, c = rc - r * n2_out;
+        if (J.rmask && !((J.rmask[r] >> J.rbit) & 1)) continue;   // row outside the group's face
         unsigned node = J.dir == 1 ? c : r;   // coarse node
         int z[D];
 #pragma unroll
@@ -1145,6 +1146,7 @@ __global__ void __launch_bounds__(256) k_jobs_pbox(JobList jl) {
         const unsigned s = t >= per_s ? 1u : 0u;
         const unsigned rc = t - s * per_s;
         const unsigned r = rc / n2_out, c = rc - r * n2_out;
+        if (J.rmask && !((J.rmask[r] >> J.rbit) & 1)) continue;   // row outside the group's face
         unsigned node = J.dir == 1 ? c : r;   // fine node
         int lo = 0, hi = 0, st = 1;
         bool mid = false;

@@ -155,6 +155,8 @@ struct Job {
     int64_t opitch = 0;   // output row pitch (0: natural n2_out)
     int box_mf = 0;       // transfer on a box lattice: fine lattice points per axis (0: use the ELL arrays)
     int box_d = 0;        // ... and its dimension (prolongation jobs, W = 2)
+    const uint8_t* rmask = nullptr;   // box transfers: only the x-rows r with bit rbit of rmask[r] set are computed
+    int rbit = 0;                     // (face groups of the cross-grid apply live on the rows of their own face)
 };
 struct JobList {
     int nj, total_blocks;

@@ -632,12 +632,15 @@ static int cross_lower_batched(sg_problem* P, const double* X, double* Y) {
     for (int pp = 1; pp <= ng; ++pp) {
         std::vector<double*> outs(nga);
         for (int o = 0; o < nga; ++o) outs[o] = Q0(pp, o);
-        SG_TRY(pass1_vgroups(P, pp, L - pp, X + A[pp - 1].off1, outs.data(), n2(L - pp)));
+        SG_TRY(pass1_vgroups(P, pp, L - pp, X + A[pp - 1].off1, outs.data(), n2(L - pp), nullptr, 0, 0, true));
     }
     // 2./3. per group: restriction chains in v and Horner prolongation in x; the last
     // Horner stage of target p (m = p) writes H[p][o] with the even pitch
     std::vector<std::vector<int64_t>> qoff(ng);
     for (int o = 0; o < nga; ++o) {
+        // boundary-only (face) groups: their intermediates are needed on the x-rows of their own face
+        // only (prolongation in x keeps a face inside itself), all other rows meet zero coefficients
+        const bool face_rows = o >= P->ng_int && nga - P->ng_int <= 8 && P->fv.kind == SG_MESH_BOX;
         int64_t pos = 0;
         for (int pp = 1; pp <= ng; ++pp) {
             qoff[pp - 1].assign(ng - pp + 1, 0);
@@ -658,6 +661,10 @@ static int cross_lower_batched(sg_problem* P, const double* X, double* Y) {
                 jobs.push_back({Q(pp, k - 1), nullptr, Q(pp, k), P->fv.lev[lf].rcols, P->fv.lev[lf].rvals, n1(pp), n2(lf),
                                 n2(lc), 1.0, 1, 1, Wv, 0});
                 if (P->fv.kind == SG_MESH_BOX) jobs.back().box_mf = P->fv.lev[lf].m;
+                if (face_rows && P->fx.lev[pp].bmask) {   // face group: rows of its own face only
+                    jobs.back().rmask = P->fx.lev[pp].bmask;
+                    jobs.back().rbit = o - P->ng_int;
+                }
             }
             SG_TRY(launch_jobs(P, jobs));
         }
@@ -675,6 +682,10 @@ static int cross_lower_batched(sg_problem* P, const double* X, double* Y) {
                 }
                 J.box_mf = P->fx.lev[m].m;   // (box factor: checked by cross_lower_batched)
                 J.box_d = P->fx.d;
+                if (face_rows && P->fx.lev[m].bmask) {
+                    J.rmask = P->fx.lev[m].bmask;
+                    J.rbit = o - P->ng_int;
+                }
                 jobs.push_back(J);
             }
             SG_TRY(launch_jobs(P, jobs));
@@ -787,9 +798,11 @@ static int cross_upper_batched(sg_problem* P, const double* X, double* Y) {
         ep.ne = 0;
         for (int a = 0; a < nxg; ++a) {
             const auto& ce = P->xgroups[a].comb[lvt][0];
-            ep.e[ep.ne++] = {H(p, a), ce.st, ce.s_out, ce.s_in, 0, 1.0};
+            // face x-groups: their chain results are exact zeros on interior x-rows (skipped there)
+            ep.e[ep.ne++] = {H(p, a), ce.st, ce.s_out, ce.s_in, P->xgroups[a].bonly ? 1 : 0, 1.0};
         }
-        SG_TRY(launch_vgat_st(P, P->fv.d, 1, n1(p), n2(lvt), P->fv.lev[lvt].so, ep, Y + A[p - 1].off1, 1.0));
+        SG_TRY(launch_vgat_st(P, P->fv.d, 1, n1(p), n2(lvt), P->fv.lev[lvt].so, ep, Y + A[p - 1].off1, 1.0,
+                              P->fx.lev[p].bflag));
     }
     return SG_OK;
 }
