@@ -130,7 +130,10 @@ struct XftTile {
     int np;                    // producer lanes (each loads 1/np of the stage box along the slowest line axis)
 };
 
-template <int D, int NGI, bool CTAB>
+// TABM: where the boundary path finds the class coefficients of the interior groups:
+//   0 whole class table in shared memory (small lattices), 1 constant bank, 2 per-tile compact
+//   table in shared memory ([3 x tile lines][NGI][W]: the classes of the tile's own target lines)
+template <int D, int NGI, int TABM>
 __global__ void __launch_bounds__(32 * 17, 1)
     k_xfanin_tma(const __grid_constant__ CUtensorMap tmap, int nga, int n2, int m, XftTile tl,
                  const double* __restrict__ tab, const __grid_constant__ XftCoef cint, double* __restrict__ Y, const double* __restrict__ skip,
@@ -148,7 +151,8 @@ __global__ void __launch_bounds__(32 * 17, 1)
     // (every coefficient is a warp-uniform broadcast load; the global table cost a 64-bit address
     // computation and an L1 lookup per multiply-add)
     double* stab = reinterpret_cast<double*>(smraw + (size_t)nst * stage_elems * 8 + 2 * (size_t)nst * sizeof(uint64_t));
-    if (!CTAB) {
+    constexpr bool CTAB = TABM != 0;
+    if (TABM == 0) {
         const int ntab = (D == 3 ? 27 : 9) * nga * G::W;
         for (int i = threadIdx.x; i < ntab; i += blockDim.x) stab[i] = __ldg(tab + i);
     }
@@ -165,6 +169,18 @@ __global__ void __launch_bounds__(32 * 17, 1)
     const int L1 = tl1 * tl.wl1 * G::B1, L2 = tl2 * tl.wl2 * G::B2;   // first target line of the tile
     const int t0 = seg * tl.seglen, t1 = min(m, t0 + tl.seglen);
     const int ts = max(t0 - 1, 0), te = min(t1, m - 1);
+    const int TL1 = tl.wl1 * G::B1, TL2 = D == 3 ? tl.wl2 * G::B2 : 1;   // target lines of the tile
+    if (TABM == 2) {
+        const int ntab = 3 * TL1 * TL2 * NGI * W;
+        for (int i = threadIdx.x; i < ntab; i += blockDim.x) {
+            const int lc = i / (NGI * W), rem = i - lc * NGI * W, g = rem / W, k = rem - g * W;
+            const int c0 = lc % 3, j1 = (lc / 3) % TL1, j2 = lc / (3 * TL1);
+            const int z1 = L1 + j1, z2 = L2 + j2;
+            const int c1 = z1 == 0 ? 0 : (z1 >= m - 1 ? 2 : 1);
+            const int c2 = D == 3 ? (z2 == 0 ? 0 : (z2 >= m - 1 ? 2 : 1)) : 0;
+            stab[i] = __ldg(tab + ((c0 + 3 * c1 + 9 * c2) * nga + g) * W + k);
+        }
+    }
     // CTA-level: are all target lines of the tile interior lines?
     const bool cta_lines_int = L1 >= 1 && L1 + tl.wl1 * G::B1 - 1 <= m - 2 &&
                                (D == 2 || (L2 >= 1 && L2 + tl.wl2 * G::B2 - 1 <= m - 2));
@@ -289,7 +305,8 @@ __global__ void __launch_bounds__(32 * 17, 1)
                 const int p = t + w - 1;
                 const int c0 = p <= 0 ? 0 : (p >= m - 1 ? 2 : 1);
                 cb[u][w] = (c0 + tcls12[u]) * nga * W;
-                cbi[u][w] = (c0 + tcls12[u]) * NGI * W;
+                cbi[u][w] = TABM == 2 ? (c0 + 3 * ((lb1 + G::u1(u)) + TL1 * (lb2 + G::u2(u)))) * NGI * W
+                                      : (c0 + tcls12[u]) * NGI * W;
             }
 #pragma unroll
         for (int g = 0; g < NGI; ++g, ++q) {
@@ -318,7 +335,7 @@ __global__ void __launch_bounds__(32 * 17, 1)
             } else {
                 // near the boundary: constant-cache table when boundary steps are a minority
                 // (m >= 9), global class table (L1 broadcast) on the tiny all-boundary lattices
-                const double* tg = CTAB ? c_xft + g * W : stab + g * W;
+                const double* tg = TABM == 1 ? c_xft + g * W : stab + g * W;
 #pragma unroll
                 for (int s = 0; s < NS; ++s)
 #pragma unroll
@@ -327,7 +344,7 @@ __global__ void __launch_bounds__(32 * 17, 1)
                         for (int k = 0; k < W; ++k)
                             if (xft::pair_ok<D>(s, u, k)) {
                                 const int slot = 1 - G::d0(k);
-                                const double cf = CTAB ? tg[cbi[u][slot] + k] : tg[cb[u][slot] + k];
+                                const double cf = TABM != 0 ? tg[cbi[u][slot] + k] : tg[cb[u][slot] + k];
                                 acc[u][slot] = fma(cf, src[s], acc[u][slot]);
                             }
             }
@@ -512,8 +529,12 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
     // 0.38 -> 0.33 ms on (3,9); the 52 KB 3D table costs too much occupancy from m = 9 on; profiles/r2r)
     const bool ctab = d == 3 ? m >= 9 : m >= 33;
     if (!ctab && d == 3) tl.nst = 3;   // room for two CTAs per SM next to the 52 KB shared-memory class table
+    // 3D tiles of 2 x 2 target lines: the 12 class rows of the tile in shared memory (14 KB)
+    // ((3,5) 1.35 -> 1.22 ms, (4,4) 1.00 -> 0.97 ms; no gain from m = 33 on; profiles/r2x)
+    const bool tile_tab = ctab && d == 3 && tl.wl1 == 1 && tl.wl2 == 1 && m <= 17;
     size_t smem = (size_t)tl.nst * stage_b + 2 * tl.nst * sizeof(uint64_t);
     if (!ctab) smem += sizeof(double) * (d == 3 ? 27 : 9) * nga * P->fx.W;
+    if (tile_tab) smem += sizeof(double) * 3 * 4 * ngi * P->fx.W;
     {
         int ncls = 1;
         for (int q = 0; q < d; ++q) ncls *= 3;
@@ -531,9 +552,9 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
         k_xfanin_tma<DD, NG, CT><<<(unsigned)nblk, threads, smem, P->stream>>>(tm, nga, (int)n2, m, tl, tab, ci, Y, P->skip, (long long)ypitch, cmk); \
     } while (0)
     if (d == 3) {
-        if (ctab) XFT(3, 10, true); else XFT(3, 10, false);
+        if (tile_tab) XFT(3, 10, 2); else if (ctab) XFT(3, 10, 1); else XFT(3, 10, 0);
     } else {
-        if (ctab) XFT(2, 6, true); else XFT(2, 6, false);
+        if (ctab) XFT(2, 6, 1); else XFT(2, 6, 0);
     }
 #undef XFT
     P->launches++;
