@@ -286,9 +286,10 @@ def roofline(res, cfg, fp):
     n_ap = max(kt["launches"], 1)
     roof = {"bound": "alu", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
             "frac": (achieved_tf / peak_tf) if achieved_tf else None, "traffic": None,
-            "kernel": ("strip-operator apply per component grid (all its kernels): pass 1 along v (k_vmom "
-                       "shifted moments / k_vfan_st stencils) + pass 2 along x (k_xfanin_tma TMA line sweep, "
-                       "k_xwhole, k_xgat_st, k_gather_s2); device globaltimer stamps around every apply"),
+            "kernel": ("strip-operator apply per component grid (all its kernels): fused k_fwhole on tiny "
+                       "x-lattices; else pass 1 along v (k_vmom shifted moments / k_vfan_st stencils) + pass 2 "
+                       "along x (k_xfanin_tma TMA line sweep, k_xwhole, k_xgat_st, k_gather_s2c / k_gather_s2); "
+                       "device globaltimer stamps around every apply"),
             "peak_source": "FP64 DFMA pipe, " + fp.get("source", ""),
             "flops_note": "2 FLOP per multiply-add on the structural nonzeros of the factor matrices "
                           "(|a_ij| > 1e-12 max|a|), face groups on boundary rows only (DESIGN.md sec. 5)",
