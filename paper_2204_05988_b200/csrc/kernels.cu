@@ -150,8 +150,8 @@ __global__ void __launch_bounds__(256) k_gather_s2(int64_t n1_in, int64_t n2_in,
 // ... the same with CPT columns per thread (columns lane, lane + 32, ... of a 32*CPT-wide tile): a warp
 // works on ONE row r, so every coefficient load (warp-uniform broadcast) feeds CPT multiply-adds
 // and the pattern row is read once per warp tile.
-template <int W, int CPT>
-__global__ void __launch_bounds__(256) k_gather_s2c(int64_t n1_in, int64_t n2_in, int64_t n1_out,
+template <int W, int CPT, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_gather_s2c(int64_t n1_in, int64_t n2_in, int64_t n1_out,
                                                     const int32_t* __restrict__ cols,
                                                     const __grid_constant__ EntryList el, double* __restrict__ out,
                                                     double beta, int ncoltiles, const double* __restrict__ skip) {
@@ -296,17 +296,18 @@ int launch_gather(sg_problem* P, int dir, int W, int S_out, int64_t n1_in, int64
         es.sbeg[0] = es.sbeg[1] = es.sbeg[2] = 0;
         if (W == 7 && n2_in >= 128) {   // (narrower grids: the flattened kernel below measured faster)
             // several columns per thread: one coefficient load per CPT multiply-adds
-            // (tile width chosen for the least padding)
-            const int64_t pad4 = (n2_in + 127) / 128 * 128, pad2 = (n2_in + 63) / 64 * 64;
-            const int cpt = pad4 <= pad2 ? 4 : 2;
+            // 4 columns per thread unless the 128-column tiles would pad the rows by more than 6 %
+            // (two CTAs per SM at 128 registers: (6,5) 1.56 -> 1.29 ms, profiles/r2z)
+            const int64_t pad4 = (n2_in + 127) / 128 * 128;
+            const int cpt = pad4 * 100 <= n2_in * 106 ? 4 : 2;
             const int64_t nct = (n2_in + 32 * cpt - 1) / (32 * cpt);
             const int64_t nblk = std::min<int64_t>((nrows_out + 7) / 8 * nct, 148 * 64);
             if (cpt == 4)
-                k_gather_s2c<7, 4><<<(unsigned)nblk, 256, 0, P->stream>>>(n1_in, n2_in, nrows_out, cols, es, out, beta,
-                                                                          (int)nct, P->skip);
+                k_gather_s2c<7, 4, 2><<<(unsigned)nblk, 256, 0, P->stream>>>(n1_in, n2_in, nrows_out, cols, es, out, beta,
+                                                                             (int)nct, P->skip);
             else
-                k_gather_s2c<7, 2><<<(unsigned)nblk, 256, 0, P->stream>>>(n1_in, n2_in, nrows_out, cols, es, out, beta,
-                                                                          (int)nct, P->skip);
+                k_gather_s2c<7, 2, 2><<<(unsigned)nblk, 256, 0, P->stream>>>(n1_in, n2_in, nrows_out, cols, es, out, beta,
+                                                                             (int)nct, P->skip);
             P->launches++;
             SG_CUDA(cudaGetLastError());
             return SG_OK;
