@@ -7,7 +7,7 @@ NVCC=${NVCC:-/usr/local/cuda/bin/nvcc}
 FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr $*"
 OBJS=""
 PIDS=""
-for f in mesh assemble kernels xfanin xfanin_tma vmoment setup solver strip_solver api; do
+for f in mesh assemble kernels xfanin xfanin_tma vmoment d1fused setup solver strip_solver api; do
   $NVCC $FLAGS -dc -o "$f.o" "$f.cu" &
   PIDS="$PIDS $!"
   OBJS="$OBJS $f.o"

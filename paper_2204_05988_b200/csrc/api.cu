@@ -216,6 +216,7 @@ extern "C" void sg_destroy(sg_problem* P) {
                     cudaFree(ce.st);
                     cudaFree(ce.ctab);
                 }
+    free_d1fused(P);
     cudaFree(P->wsZ); cudaFree(P->wsA); cudaFree(P->wsB); cudaFree(P->wsH); cudaFree(P->red); cudaFree(P->scal);
     cudaFree(P->cross_q); cudaFree(P->cross_h);
     for (double* t : P->xfi_tab) cudaFree(t);

@@ -293,6 +293,12 @@ struct sg_problem {
     std::vector<double*> fw_dev;
     int fw_np = 0;
     bool use_fused = true;
+    // fused batched apply for d = 1 (d1fused.cu): per-level device tables
+    bool d1_ok = false;
+    std::vector<double**> d1_bst;   // [l2] -> [nb] stencil-format v matrices
+    std::vector<void*> d1_ent;      // [l1] -> entries grouped by v-group
+    std::vector<int*> d1_ebeg;      // [l1] -> [nb + 1] entry ranges
+    std::vector<int> d1_nent;
     // L2-resident column chunks of the two-pass apply: intermediates per chunk (bytes; 0 = off)
     int64_t l2_chunk_bytes = 0;
     int64_t l2_chunk_mincols = 64;
@@ -361,6 +367,13 @@ int launch_xwhole(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pitch, 
 int prepare_fwhole(sg_problem* P);
 
 int launch_fwhole(sg_problem* P, int l1, int l2, int64_t n2, const double* X, double* Y);
+// d1fused.cu
+int prepare_d1fused(sg_problem* P);
+void free_d1fused(sg_problem* P);
+int launch_d1fused(sg_problem* P, int n, const Grid* const* grids, const double* const* X, double* const* Y,
+                   const double* const* skips, double* fbytes);
+int launch_tstamp_batch(sg_problem* P, int n, const double* const* skips, const double* bytes, const double* flops);
+double apply_flops(const sg_problem* P, const Grid& g);
 // vmoment.cu
 int prepare_vmom(sg_problem* P);
 int launch_vmom(sg_problem* P, int l2, int64_t nrows, int64_t n2, int64_t pitch, const double* X, double* const* outs,

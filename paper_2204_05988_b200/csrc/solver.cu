@@ -44,6 +44,8 @@ static double diag_flops(const sg_problem* P, const Grid& g) {
     return f;
 }
 
+double apply_flops(const sg_problem* P, const Grid& g) { return diag_flops(P, g); }
+
 static bool l_has_xfi(const sg_problem* P, int l1) {
     return P->use_tma && l1 < (int)P->xfi_tab.size() && P->xfi_tab[l1] != nullptr &&
            ((P->fx.d == 3 && P->ng_int == 10) || (P->fx.d == 2 && P->ng_int == 6)) && P->fx.lev[l1].m >= 3;
@@ -139,6 +141,12 @@ static int apply_diag_impl(sg_problem* P, const Grid& g, const double* X, double
     const int nb = (int)P->vorder.size();
     const bool vbox = P->fv.kind == SG_MESH_BOX && nb <= MAXG;
     const bool xbox = P->fx.kind == SG_MESH_BOX;
+    // ---- d = 1: fused two-sided kernel (one node per thread, 3 x 3 neighbourhood), no intermediates
+    if (P->d1_ok) {
+        const Grid* gp = &g;
+        const double* sk = P->skip;
+        return launch_d1fused(P, 1, &gp, &X, &Y, &sk, fbytes);
+    }
     // ---- fused single pass (tiny x-lattices): no intermediates
     {
         const int rc = launch_fwhole(P, g.l1, g.l2, g.n2, X, Y);
@@ -463,6 +471,7 @@ int prepare_stencils(sg_problem* P) {
     SG_TRY(prepare_xfanin(P));
     SG_TRY(prepare_vmom(P));
     SG_TRY(prepare_fwhole(P));
+    SG_TRY(prepare_d1fused(P));
     SG_CUDA(cudaStreamSynchronize(P->stream));
     return SG_OK;
 }

@@ -676,6 +676,35 @@ static int enqueue_bicgstab(sg_problem* P, bool graph, const Conds& cd, const do
     // all grids' applies of one half-iteration: serial on P->stream, or (small configurations)
     // forked onto one stream per grid with private workspaces and joined again
     auto applies = [&](const double* in, double* out) -> int {
+        if (P->d1_ok) {
+            // d = 1: every grid's fused apply in ONE launch (per-grid convergence flags inside)
+            const int n = (int)gr.size();
+            std::vector<const double*> xs(n), sk(n);
+            std::vector<double*> ys(n);
+            std::vector<double> by(n, 0.0), fl(n, 0.0);
+            if (P->timing) {
+                k_tstamp<<<1, 1, 0, P->stream>>>(P->ctl, nullptr, P->stamp_slot, 0, 0.0, 0.0);
+                P->launches++;
+            }
+            for (int i = 0; i < n; ++i) {
+                xs[i] = in + offs[i];
+                ys[i] = out + offs[i];
+                sk[i] = P->scal + i * NSC + 5;
+            }
+            for (int i = 0; i < n; ++i) {   // (factor bytes per grid for the roofline accounting)
+                double fb = 0.0;
+                if (P->timing) {
+                    const double* x1 = xs[i];
+                    (void)x1;
+                    fb = 8.0 * 3 * ((double)P->vorder.size() * gr[i]->n2 + P->d1_nent[gr[i]->l1] * (double)gr[i]->n1);
+                    by[i] = 16.0 * S * (double)gsize(*gr[i]) + fb;
+                    fl[i] = apply_flops(P, *gr[i]);
+                }
+            }
+            SG_TRY(launch_d1fused(P, n, gr.data(), xs.data(), ys.data(), sk.data(), nullptr));
+            if (P->timing) SG_TRY(launch_tstamp_batch(P, n, sk.data(), by.data(), fl.data()));
+            return SG_OK;
+        }
         if (!P->par_applies) {
             for (size_t i = 0; i < gr.size(); ++i)
                 SG_TRY(apply_diag(P, *gr[i], in + offs[i], out + offs[i], P->scal + i * NSC + 5));
