@@ -133,8 +133,9 @@ struct XftTile {
 // TABM: where the boundary path finds the class coefficients of the interior groups:
 //   0 whole class table in shared memory (small lattices), 1 constant bank, 2 per-tile compact
 //   table in shared memory ([3 x tile lines][NGI][W]: the classes of the tile's own target lines)
-template <int D, int NGI, int TABM>
-__global__ void __launch_bounds__(32 * 17, 1)
+// CPT: v-columns per lane (2: adjacent columns, 128-bit stage loads; every coefficient load feeds 2 multiply-adds)
+template <int D, int NGI, int TABM, int CPT = 1>
+__global__ void __launch_bounds__(CPT == 2 ? 32 * 9 : 32 * 17, 1)
     k_xfanin_tma(const __grid_constant__ CUtensorMap tmap, int nga, int n2, int m, XftTile tl,
                  const double* __restrict__ tab, const __grid_constant__ XftCoef cint, double* __restrict__ Y, const double* __restrict__ skip,
                  long long ypitch, const __grid_constant__ XftMask cmask) {
@@ -258,8 +259,10 @@ __global__ void __launch_bounds__(32 * 17, 1)
     // ---------------- consumers: warp -> (column group, warp block of lines)
     const int wc = warp % tl.wc, wl = warp / tl.wc;
     const int wl1 = wl % tl.wl1, wl2 = wl / tl.wl1;
-    const int col = ct * tl.bc + wc * 32 + lane;
-    const bool cval = col < n2;
+    const int col = ct * tl.bc + (wc * 32 + lane) * CPT;
+    bool cval[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) cval[c] = col + c < n2;
     const int lb1 = wl1 * G::B1, lb2 = wl2 * G::B2;   // warp's first target line inside the tile
     // stage offsets of the warp's source lines (local halo coordinates)
     int soff[NS];
@@ -267,7 +270,7 @@ __global__ void __launch_bounds__(32 * 17, 1)
     for (int s = 0; s < NS; ++s) {
         const int le1 = lb1 + (s % G::NE1);                 // (lb1 + e1r + 1), e1r = s%NE1 - 1
         const int le2 = D == 3 ? lb2 + (s / G::NE1) : 0;
-        soff[s] = (le2 * tl.e1 + le1) * tl.bc + wc * 32 + lane;
+        soff[s] = (le2 * tl.e1 + le1) * tl.bc + (wc * 32 + lane) * CPT;
     }
     int tline[NT], tcls12[NT];
     bool tval[NT];
@@ -288,9 +291,24 @@ __global__ void __launch_bounds__(32 * 17, 1)
         if (tval[u])
 #pragma unroll
             for (int c0 = 0; c0 < 3; ++c0) wm[c0] |= cmask.m[c0 + tcls12[u]];
-    double acc[NT][3];
+    double acc[NT][3][CPT];
 #pragma unroll
-    for (int u = 0; u < NT; ++u) acc[u][0] = acc[u][1] = acc[u][2] = 0.0;
+    for (int u = 0; u < NT; ++u)
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) acc[u][0][c] = acc[u][1][c] = acc[u][2][c] = 0.0;
+    auto load_src = [&](const double* st, double (&src)[NS][CPT]) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+            if (xft::src_used<D>(s)) {
+                if (CPT == 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(st + soff[s]);
+                    src[s][0] = v.x;
+                    src[s][CPT - 1] = v.y;
+                } else {
+                    src[s][0] = st[soff[s]];
+                }
+            }
+    };
 
     int q = 0, cbuf = 0;
     uint32_t cph = 0;
@@ -317,10 +335,8 @@ __global__ void __launch_bounds__(32 * 17, 1)
                 cph ^= 1u;
             }
             const double* st = stages + (size_t)b * stage_elems;
-            double src[NS];
-#pragma unroll
-            for (int s = 0; s < NS; ++s)
-                if (xft::src_used<D>(s)) src[s] = st[soff[s]];
+            double src[NS][CPT];
+            load_src(st, src);
             if (wint) {
 #pragma unroll
                 for (int s = 0; s < NS; ++s)
@@ -330,7 +346,8 @@ __global__ void __launch_bounds__(32 * 17, 1)
                         for (int k = 0; k < W; ++k)
                             if (xft::pair_ok<D>(s, u, k)) {
                                 const int slot = 1 - G::d0(k);
-                                acc[u][slot] = fma(cint.c[g][k], src[s], acc[u][slot]);
+#pragma unroll
+                                for (int c = 0; c < CPT; ++c) acc[u][slot][c] = fma(cint.c[g][k], src[s][c], acc[u][slot][c]);
                             }
             } else {
                 // near the boundary: constant-cache table when boundary steps are a minority
@@ -345,7 +362,8 @@ __global__ void __launch_bounds__(32 * 17, 1)
                             if (xft::pair_ok<D>(s, u, k)) {
                                 const int slot = 1 - G::d0(k);
                                 const double cf = TABM != 0 ? tg[cbi[u][slot] + k] : tg[cb[u][slot] + k];
-                                acc[u][slot] = fma(cf, src[s], acc[u][slot]);
+#pragma unroll
+                                for (int c = 0; c < CPT; ++c) acc[u][slot][c] = fma(cf, src[s][c], acc[u][slot][c]);
                             }
             }
             __syncwarp();
@@ -364,10 +382,8 @@ __global__ void __launch_bounds__(32 * 17, 1)
                 if ((wm_t >> (g - NGI)) & 1u) {
                     const double* st = stages + (size_t)b * stage_elems;
                     const double* tg = CTAB ? tab + g * W : stab + g * W;
-                    double src[NS];
-#pragma unroll
-                    for (int s = 0; s < NS; ++s)
-                        if (xft::src_used<D>(s)) src[s] = st[soff[s]];
+                    double src[NS][CPT];
+                    load_src(st, src);
 #pragma unroll
                     for (int s = 0; s < NS; ++s)
 #pragma unroll
@@ -376,8 +392,9 @@ __global__ void __launch_bounds__(32 * 17, 1)
                             for (int k = 0; k < W; ++k)
                                 if (xft::pair_ok<D>(s, u, k)) {
                                     const int slot = 1 - G::d0(k);
-                                    acc[u][slot] = fma(CTAB ? __ldg(tg + cb[u][slot] + k) : tg[cb[u][slot] + k], src[s],
-                                                       acc[u][slot]);
+                                    const double cf = CTAB ? __ldg(tg + cb[u][slot] + k) : tg[cb[u][slot] + k];
+#pragma unroll
+                                    for (int c = 0; c < CPT; ++c) acc[u][slot][c] = fma(cf, src[s][c], acc[u][slot][c]);
                                 }
                 }
                 __syncwarp();
@@ -385,22 +402,29 @@ __global__ void __launch_bounds__(32 * 17, 1)
             }
         }
         // target t-1 complete
-        if (t - 1 >= t0 && cval) {
+        if (t - 1 >= t0) {
 #pragma unroll
             for (int u = 0; u < NT; ++u)
-                if (tval[u]) Y[((long long)(t - 1) + (long long)m * tline[u]) * ypitch + col] = acc[u][0];
-        }
 #pragma unroll
-        for (int u = 0; u < NT; ++u) {
-            acc[u][0] = acc[u][1];
-            acc[u][1] = acc[u][2];
-            acc[u][2] = 0.0;
+                for (int c = 0; c < CPT; ++c)
+                    if (tval[u] && cval[c])
+                        Y[((long long)(t - 1) + (long long)m * tline[u]) * ypitch + col + c] = acc[u][0][c];
         }
-    }
-    if (t1 == m && cval) {
 #pragma unroll
         for (int u = 0; u < NT; ++u)
-            if (tval[u]) Y[((long long)(m - 1) + (long long)m * tline[u]) * ypitch + col] = acc[u][0];
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                acc[u][0][c] = acc[u][1][c];
+                acc[u][1][c] = acc[u][2][c];
+                acc[u][2][c] = 0.0;
+            }
+    }
+    if (t1 == m) {
+#pragma unroll
+        for (int u = 0; u < NT; ++u)
+#pragma unroll
+            for (int c = 0; c < CPT; ++c)
+                if (tval[u] && cval[c]) Y[((long long)(m - 1) + (long long)m * tline[u]) * ypitch + col + c] = acc[u][0][c];
     }
 }
 
@@ -420,21 +444,21 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // tile choice: minimise TMA source-line loads per valid target line
 constexpr int XFT_MINW = 4;   // at least 4 consumer warps per CTA
-static XftTile choose_tile(int d, int m, int64_t n2, int force_wc, int box_kb) {
+static XftTile choose_tile(int d, int m, int64_t n2, int force_wc, int box_kb, int cpt = 1, int max_nw = 16) {
     XftTile best{};
     double best_cost = 1e30;
     const int B1 = d == 3 ? 2 : 4;
     const int lines1 = m, lines2 = d == 3 ? m : 1;
     for (int wc = 1; wc <= 8; wc *= 2) {
         if (wc == 8 && force_wc != 8) continue;
-        if (wc > 1 && n2 < 32LL * wc) continue;
+        if (wc > 1 && n2 < 32LL * wc * cpt) continue;
         if (force_wc > 0 && wc != force_wc) continue;
         for (int w1 = 1; w1 <= 16; ++w1)
             for (int w2 = 1; w2 <= (d == 3 ? 16 : 1); ++w2) {
                 const int nw = w1 * w2 * wc;
-                if (nw < XFT_MINW || nw > 16) continue;
+                if (nw < XFT_MINW || nw > max_nw) continue;
                 const int e1 = w1 * B1 + 2, e2 = d == 3 ? w2 * 2 + 2 : 1;
-                const int bc = 32 * wc;
+                const int bc = 32 * wc * cpt;
                 if ((double)e1 * e2 * bc * 8 > box_kb * 1024.0) continue;
                 const int nt1 = (lines1 + w1 * B1 - 1) / (w1 * B1);
                 const int nt2 = d == 3 ? (lines2 + w2 * 2 - 1) / (w2 * 2) : 1;
@@ -476,7 +500,23 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
     // on those lattices: more independent TMA producers per SM (grid (3,5): 2.02 -> 1.82 ms)
     // (round-2 sweeps profiles/r2g, r2m: 4x6 / 4x8 / 6x6-line boxes with 2-6 stages are equal or slower)
     const int box_kb = wc_auto ? (d == 3 ? (wc_auto == 8 ? 32 : 16) : 8) : 24;
-    XftTile tl = choose_tile(d, m, n2, wc_auto, box_kb);
+    // two columns per lane on the wide 3D tiles: (4,4) 0.98 -> 0.85 ms, (3,5) 1.23 -> 1.06 ms (profiles/r2D)
+    // (and on the other families with at least 64 columns: configs[2] (6,6) 0.25 -> 0.21 ms, (7,5) 0.32 ->
+    // 0.26 ms; configs[4] (6,2) 1.30 -> 1.24 ms)
+    int cpt = (d == 3 && wc_auto == 8) ? 2 : 1;
+    XftTile tl{};
+    if (cpt == 2) {
+        tl = choose_tile(d, m, n2, 4, box_kb, 2, 8);
+    } else if (m >= 9 && n2 >= 64 && (d == 2 || wc_auto == 0)) {
+        cpt = 2;
+        tl = d == 2 ? choose_tile(d, m, n2, n2 >= 256 ? 4 : (n2 >= 128 ? 2 : 1), 16, 2, 8) : choose_tile(d, m, n2, 0, 40, 2, 8);
+        if (tl.nw == 0) {
+            cpt = 1;
+            tl = choose_tile(d, m, n2, wc_auto, box_kb);
+        }
+    } else {
+        tl = choose_tile(d, m, n2, wc_auto, box_kb);
+    }
     if (tl.nw == 0) tl = choose_tile(d, m, n2, 0, 24);
     // split the sweep until there are >= 2 CTAs per SM
     const int64_t base = (int64_t)tl.ntl1 * tl.ntl2 * tl.nct;
@@ -520,7 +560,7 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
     const size_t stage_b = (size_t)tl.e1 * tl.e2 * tl.bc * 8;
     // 4 stages measured best (deeper rings shrink L1 and were slower: (2,6) 3.3 -> 5.1 ms at 8 stages)
     // (3 stages on the wide-box 3D tiles: 1.2 % faster than 4)
-    tl.nst = wc_auto && d == 3 ? 3 : 4;
+    tl.nst = (wc_auto || cpt == 2) && d == 3 ? 3 : 4;
     if (P->verbose)
         fprintf(stderr, "xft l1=%d m=%d n2=%lld tile w1=%d w2=%d wc=%d nw=%d box=%dx%dx%d nst=%d seglen=%d np=%d nblk=%lld\n", l1, m,
                 (long long)n2, tl.wl1, tl.wl2, tl.wc, tl.nw, tl.e1, tl.e2, tl.bc, tl.nst, tl.seglen, tl.np, (long long)nblk);
@@ -546,15 +586,17 @@ int launch_xfanin_tma(sg_problem* P, int l1, int64_t n1, int64_t n2, int64_t pit
     }
     const int threads = 32 * (tl.nw + 1);
     const double* tab = P->xfi_tab[l1];
-#define XFT(DD, NG, CT)                                                                                          \
+#define XFT(DD, NG, ...)                                                                                          \
     do {                                                                                                         \
-        cudaFuncSetAttribute(k_xfanin_tma<DD, NG, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-        k_xfanin_tma<DD, NG, CT><<<(unsigned)nblk, threads, smem, P->stream>>>(tm, nga, (int)n2, m, tl, tab, ci, Y, P->skip, (long long)ypitch, cmk); \
+        cudaFuncSetAttribute(k_xfanin_tma<DD, NG, __VA_ARGS__>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        k_xfanin_tma<DD, NG, __VA_ARGS__><<<(unsigned)nblk, threads, smem, P->stream>>>(tm, nga, (int)n2, m, tl, tab, ci, Y, P->skip, (long long)ypitch, cmk); \
     } while (0)
     if (d == 3) {
-        if (tile_tab) XFT(3, 10, 2); else if (ctab) XFT(3, 10, 1); else XFT(3, 10, 0);
+        if (cpt == 2 && tile_tab) XFT(3, 10, 2, 2); else if (cpt == 2 && ctab) XFT(3, 10, 1, 2);
+        else if (tile_tab) XFT(3, 10, 2); else if (ctab) XFT(3, 10, 1); else XFT(3, 10, 0);
     } else {
-        if (ctab) XFT(2, 6, 1); else XFT(2, 6, 0);
+        if (cpt == 2 && ctab) XFT(2, 6, 1, 2); else if (cpt == 2) XFT(2, 6, 0, 2);
+        else if (ctab) XFT(2, 6, 1); else XFT(2, 6, 0);
     }
 #undef XFT
     P->launches++;
